@@ -1,0 +1,629 @@
+/*
+ * glint_oracle.c -- CPU ORACLE for the per-pixel glint BRDF (arXiv 2306.05051).
+ *
+ * TEST INFRASTRUCTURE ONLY: loaded by tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs; never by the product path.
+ * It shares no code, header, table or constant generator with the CUDA path.
+ *
+ * The method is a stochastic approximation with discrete choices, so there is
+ * no closed-form "answer" to compare with: this file follows the paper's
+ * algorithm step by step, in the paper's order and notation (S1..S9 of
+ * DESIGN.md §2), taking DESIGN.md §5's reading wherever the paper is silent.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fno-tree-vectorize
+ * (no contraction: every fp32 op rounds exactly as DESIGN.md §4 writes it; fmaf
+ * appears only where the contract says fma).
+ *
+ * Citations: P:Lnnn = line of /root/reference/PAPER.md.
+ */
+#include "glint_oracle.h"
+
+#include <math.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------------- */
+/* fp32 bit helpers                                                         */
+/* ---------------------------------------------------------------------- */
+static uint32_t f2u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+static float u2f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+/* 2^k as an fp32, k in [-126, 127] (exact) */
+static float pow2i(int32_t k) { return u2f((uint32_t)(k + 127) << 23); }
+
+/* ---------------------------------------------------------------------- */
+/* Tables ("a small texture of random numbers that we precompute")  */
+/* ---------------------------------------------------------------------- */
+static float g_z[ORC_ZQ];      /* Z[k] = fp32(Phi^-1((k + 1/2) / Q))   (reading R-2) */
+static float g_cos[ORC_NANG];  /* fp32(cos(m pi / 256))  (orientation phi_j, Fig. 6) */
+static float g_sin[ORC_NANG];
+static int g_init = 0;
+
+/* standard normal CDF, fp64: Phi(x) = erfc(-x / sqrt 2) / 2 */
+static double phi_cdf(double x) { return 0.5 * erfc(-x / sqrt(2.0)); }
+
+/* Phi^-1 by plain bisection to full double resolution (slow, obviously correct). */
+static double phi_inv_bisect(double q) {
+  double lo = -40.0, hi = 40.0;
+  for (int it = 0; it < 400; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (mid == lo || mid == hi) break;
+    if (phi_cdf(mid) < q) lo = mid; else hi = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+int orc_init(void) {
+  if (g_init) return 0;
+  for (int k = 0; k < ORC_ZQ; ++k)
+    g_z[k] = (float)phi_inv_bisect(((double)k + 0.5) / (double)ORC_ZQ);
+  for (int m = 0; m < ORC_NANG; ++m) {
+    g_cos[m] = (float)cos((double)m * M_PI / 256.0);
+    g_sin[m] = (float)sin((double)m * M_PI / 256.0);
+  }
+  g_init = 1;
+  return 0;
+}
+const float* orc_ztable(void) { orc_init(); return g_z; }
+const float* orc_costable(void) { orc_init(); return g_cos; }
+const float* orc_sintable(void) { orc_init(); return g_sin; }
+
+/* ---------------------------------------------------------------------- */
+/* Contract transcendentals. IEEE + - * / sqrt, fmaf only.  */
+/* ---------------------------------------------------------------------- */
+
+/* 2^y for y <= 0 (used for (1-p)^N = 2^(N log2(1-p)), Eq. 16, and Beckmann
+ * exp). k = floor(y + 1/2), f = y - k in [-1/2, 1/2], degree-7 Taylor
+ * of e^(f ln2) in Horner form, times 2^k. y < -125 -> 0. */
+float orc_exp2(float y) {
+  if (!(y >= -125.0f)) return 0.0f;
+  float k = floorf(y + 0.5f);
+  float f = y - k;
+  float q = 0x1.ffcbfcp-17f;           /* ln2^7/7! */
+  q = fmaf(q, f, 0x1.430912p-13f);     /* ln2^6/6! */
+  q = fmaf(q, f, 0x1.5d87fep-10f);     /* ln2^5/5! */
+  q = fmaf(q, f, 0x1.3b2ab6p-7f);      /* ln2^4/4! */
+  q = fmaf(q, f, 0x1.c6b08ep-5f);      /* ln2^3/3! */
+  q = fmaf(q, f, 0x1.ebfbe0p-3f);      /* ln2^2/2! */
+  q = fmaf(q, f, 0x1.62e430p-1f);      /* ln2 */
+  q = fmaf(q, f, 1.0f);
+  return q * pow2i((int32_t)k);
+}
+
+/* atanh(s)/s = 1 + s^2/3 + s^4/5 + ... + s^14/15 (Horner in z = s^2) */
+static float atanh_series(float s) {
+  float z = s * s;
+  float q = 0x1.111112p-4f;            /* 1/15 */
+  q = fmaf(q, z, 0x1.3b13b2p-4f);      /* 1/13 */
+  q = fmaf(q, z, 0x1.745d18p-4f);      /* 1/11 */
+  q = fmaf(q, z, 0x1.c71c72p-4f);      /* 1/9 */
+  q = fmaf(q, z, 0x1.24924ap-3f);      /* 1/7 */
+  q = fmaf(q, z, 0x1.99999ap-3f);      /* 1/5 */
+  q = fmaf(q, z, 0x1.555556p-2f);      /* 1/3 */
+  q = fmaf(q, z, 1.0f);
+  return s * q;
+}
+
+/* log2(1 - p) for p in (0, 1): log(1-p) = -2 atanh(p / (2 - p)) for p < 1/2;
+ * otherwise 1 - p (exact) = 2^e m, m in [2/3, 4/3], log2 = e + 2 atanh((m-1)/(m+1))/ln2. */
+float orc_log2_1mp(float p) {
+  if (p < 0.5f) {
+    float s = p / (2.0f - p);
+    return -(atanh_series(s) * 0x1.715476p+1f); /* 2/ln2 */
+  }
+  float q = 1.0f - p;
+  uint32_t b = f2u(q);
+  int32_t e = (int32_t)((b >> 23) & 255u) - 127;
+  float m = u2f((b & 0x7FFFFFu) | 0x3F800000u); /* [1, 2) */
+  if (m > 0x1.555556p+0f) { m = m * 0.5f; e = e + 1; }
+  float s = (m - 1.0f) / (m + 1.0f);
+  return fmaf(atanh_series(s), 0x1.715476p+1f, (float)e);
+}
+
+/* atan2(y, x) in turns, in (-1/2, 1/2]. t = min/max in [0,1]; if t > tan(pi/8)
+ * reduce t' = (t-1)/(t+1) (+1/8 turn); odd Taylor series to t^17, coefficients
+ * fp32((-1)^k / ((2k+1) 2pi)); octant/quadrant fix-ups are exact in turns. */
+float orc_atan2_turns(float y, float x) {
+  float ax = fabsf(x), ay = fabsf(y);
+  float mx = ax > ay ? ax : ay;
+  float mn = ax > ay ? ay : ax;
+  if (mx == 0.0f) return 0.0f;
+  float t = mn / mx;
+  float base = 0.0f;
+  if (t > 0x1.a8279ap-2f) { t = (t - 1.0f) / (t + 1.0f); base = 0.125f; }
+  float z = t * t;
+  float q = 0x1.32c69ep-7f;
+  q = fmaf(q, z, -0x1.5bade6p-7f);
+  q = fmaf(q, z, 0x1.912b1cp-7f);
+  q = fmaf(q, z, -0x1.da1bacp-7f);
+  q = fmaf(q, z, 0x1.21bb94p-6f);
+  q = fmaf(q, z, -0x1.748376p-6f);
+  q = fmaf(q, z, 0x1.04c26cp-5f);
+  q = fmaf(q, z, -0x1.b2995ep-5f);
+  q = fmaf(q, z, 0x1.45f306p-3f);
+  float a = fmaf(t, q, base);
+  if (ay > ax) a = 0.25f - a;
+  if (x < 0.0f) a = 0.5f - a;
+  if (y < 0.0f) a = -a;
+  return a;
+}
+
+/* ---------------------------------------------------------------------- */
+/* Hash ("random seeds theta are distributed in a spatial and angular
+ * grid"; reading R-23). Published "lowbias32" integer mixer.                */
+/* ---------------------------------------------------------------------- */
+uint32_t orc_lowbias32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+/* ---------------------------------------------------------------------- */
+/* S1  Footprint: "we use screen-space derivatives to obtain the
+ * minor/major axis"; phi = orientation of the major axis v0, r = |v0|/|v1|.
+ * Reading R-7/R-8: P = |det J|, M = J J^T, lambda+ = major eigenvalue,
+ * r = lambda+ / P = sigma_max/sigma_min, psi = phi/pi = atan2(2b, a-c)/(2pi) mod 1.
+ * duv = (du/dx, dv/dx, du/dy, dv/dy). Returns 0 if degenerate.              */
+/* ---------------------------------------------------------------------- */
+int orc_footprint(const float duv[4], float* P, float* r, float* psi) {
+  float dudx = duv[0], dvdx = duv[1], dudy = duv[2], dvdy = duv[3];
+  float det = dudx * dvdy - dvdx * dudy;
+  float a = dudx * dudx + dudy * dudy;
+  float b = dudx * dvdx + dudy * dvdy;
+  float c = dvdx * dvdx + dvdy * dvdy;
+  float hm = 0.5f * (a - c);
+  float disc = sqrtf(hm * hm + b * b);
+  float lam = 0.5f * (a + c) + disc;
+  *P = fabsf(det);
+  *r = lam / *P;
+  float at = orc_atan2_turns(2.0f * b, a - c);
+  float ps = at < 0.0f ? at + 1.0f : at;
+  if (ps >= 1.0f) ps = 0.0f;
+  *psi = ps;
+  /* reading R-25: valid footprint area is [2^-64, 2^64) */
+  return (*P >= 0x1p-64f && *P < 0x1p64f) ? 1 : 0;
+}
+
+/* ---------------------------------------------------------------------- */
+/* S2  Lattice location: scale enclosure (Eq. 13, reading R-5),
+ * ratio levels and orientation bins that refine per ratio level (P:L635,
+ * Fig. 6, readings R-9/R-10), pentagon -> 3 triangles and prism ->
+ * 3 tetrahedra (Fig. 7 edges P:L804-807, readings R-11..R-13).
+ * Output: 4 grid vertices (ls = log2 texel area, lr = ratio level, jo =
+ * orientation index) with distribution weights w (Eq. 10 generalised to 4
+ * areas, "distributing over more than 2 areas").                     */
+/* ---------------------------------------------------------------------- */
+typedef struct { int32_t lr, jo; float w; } tri_vtx;
+
+int orc_lattice(float P, float r, float psi, int32_t K, int32_t ls[4], int32_t lr[4],
+                int32_t jo[4], float w[4], uint32_t* flags) {
+  /* scale: P = 2^es (1 + ts); bottom level es, top level es + 1 (Eq. 13 with
+   * the power-of-two tie resolved as reading R-5): w_top = ts (Eq. 10). */
+  uint32_t pb = f2u(P);
+  int32_t es = (int32_t)((pb >> 23) & 255u) - 127;
+  float ts = u2f((pb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+
+  /* ratio: r = 2^er (1 + tr), er in [0, K-1]; r >= 2^K -> (K-1, 1) (R-25) */
+  int32_t er;
+  float tr;
+  if (!(r >= 1.0f)) r = 1.0f;
+  if (r >= pow2i(K)) {
+    if (r > pow2i(K)) *flags |= ORC_FLAG_RATIO_CLAMPED;
+    er = K - 1;
+    tr = 1.0f;
+  } else {
+    uint32_t rb = f2u(r);
+    er = (int32_t)((rb >> 23) & 255u) - 127;
+    tr = u2f((rb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+  }
+
+  /* orientation: ring er has 2^er vertices at psi = j / 2^er (R-9) */
+  float A = psi * pow2i(er);
+  float jf = floorf(A);
+  float a = A - jf;
+  int32_t j = (int32_t)jf;
+  int32_t nI = 1 << er, nO = 2 << er;
+  tri_vtx A00 = {er, j, 0.0f}, A01 = {er, (j + 1) & (nI - 1), 0.0f};
+  tri_vtx A10 = {er + 1, 2 * j, 0.0f}, A11 = {er + 1, 2 * j + 1, 0.0f};
+  tri_vtx A12 = {er + 1, (2 * j + 2) & (nO - 1), 0.0f};
+
+  /* pentagon (tr, a) with A00=(0,0) A01=(0,1) A10=(1,0) A11=(1,1/2) A12=(1,1):
+   * T0 = {A00,A10,A11}, T1 = {A00,A11,A01}, T2 = {A01,A11,A12} (reading R-11) */
+  tri_vtx v[3];
+  float ht = 0.5f * tr;
+  if (a <= ht) {
+    v[0] = A00; v[1] = A10; v[2] = A11;
+    v[0].w = 1.0f - tr;
+    v[2].w = a + a;
+    v[1].w = tr - v[2].w;
+  } else if (a >= 1.0f - ht) {
+    float om = 1.0f - a;
+    v[0] = A01; v[1] = A11; v[2] = A12;
+    v[0].w = 1.0f - tr;
+    v[1].w = om + om;
+    v[2].w = tr - v[1].w;
+  } else {
+    v[0] = A00; v[1] = A11; v[2] = A01;
+    v[0].w = (1.0f - a) - ht;
+    v[1].w = tr;
+    v[2].w = a - ht;
+  }
+
+  /* merge coincident grid vertices (ring 0: A00 == A01, A10 == A12; R-13) */
+  for (int p = 0; p < 3; ++p)
+    for (int q = p + 1; q < 3; ++q)
+      if (v[p].lr == v[q].lr && v[p].jo == v[q].jo) { v[p].w = v[p].w + v[q].w; v[q].w = 0.0f; }
+
+  /* global vertex order by key (lr, jo), stable (R-12) */
+#define KEY(t) (((t).lr << 9) | (t).jo)
+#define CSWAP(p, q) if (KEY(v[p]) > KEY(v[q])) { tri_vtx tmp_ = v[p]; v[p] = v[q]; v[q] = tmp_; }
+  CSWAP(0, 1);
+  CSWAP(1, 2);
+  CSWAP(0, 1);
+#undef CSWAP
+#undef KEY
+
+  /* prism (triangle x [es, es+1]) -> 3 tetrahedra, staircase fill of the top
+   * level in global order (R-12); t = ts */
+  float al = v[0].w, be = v[1].w, ga = v[2].w;
+  float t = ts;
+  float ab = al + be;
+  if (t <= al) {
+    ls[0] = es;     lr[0] = v[0].lr; jo[0] = v[0].jo; w[0] = al - t;
+    ls[1] = es;     lr[1] = v[1].lr; jo[1] = v[1].jo; w[1] = be;
+    ls[2] = es;     lr[2] = v[2].lr; jo[2] = v[2].jo; w[2] = ga;
+    ls[3] = es + 1; lr[3] = v[0].lr; jo[3] = v[0].jo; w[3] = t;
+  } else if (t <= ab) {
+    ls[0] = es;     lr[0] = v[1].lr; jo[0] = v[1].jo; w[0] = ab - t;
+    ls[1] = es;     lr[1] = v[2].lr; jo[1] = v[2].jo; w[1] = ga;
+    ls[2] = es + 1; lr[2] = v[0].lr; jo[2] = v[0].jo; w[2] = al;
+    ls[3] = es + 1; lr[3] = v[1].lr; jo[3] = v[1].jo; w[3] = t - al;
+  } else {
+    ls[0] = es;     lr[0] = v[2].lr; jo[0] = v[2].jo; w[0] = 1.0f - t;
+    ls[1] = es + 1; lr[1] = v[0].lr; jo[1] = v[0].jo; w[1] = al;
+    ls[2] = es + 1; lr[2] = v[1].lr; jo[2] = v[1].jo; w[2] = be;
+    ls[3] = es + 1; lr[3] = v[2].lr; jo[3] = v[2].jo; w[3] = (t - al) - be;
+  }
+  (void)ga;
+  return 0;
+}
+
+/* ---------------------------------------------------------------------- */
+/* S3  Anisotropic grid transform (Eq. 12, reading R-14):
+ * rotate by phi_j = m pi / 256 (m = jo 2^(8-lr)), then area-preserving stretch:
+ * x = (c u + s v) 2^(-(ls+lr)/2), y = (c v - s u) 2^((lr-ls)/2).             */
+/* ---------------------------------------------------------------------- */
+static float pow2half(int32_t e) { /* 2^(e/2): odd e -> fp32(sqrt 2) * 2^floor(e/2) */
+  int32_t h = e >> 1;  /* arithmetic shift = floor */
+  float s = pow2i(h);
+  return (e & 1) ? s * 0x1.6a09e6p+0f : s;
+}
+
+void orc_grid_uv(float u, float v, int32_t ls, int32_t lr, int32_t jo, float* x, float* y) {
+  orc_init();
+  int32_t m = jo << (8 - lr);
+  float c = g_cos[m], s = g_sin[m];
+  float xr = fmaf(c, u, s * v);
+  float yr = fmaf(c, v, -(s * u));
+  *x = xr * pow2half(-(ls + lr));
+  *y = yr * pow2half(lr - ls);
+}
+
+/* S3  Simplex surface grid (Fig. 8 shear P:L882, reading R-15):
+ * lattice coordinates (x + y/2, y); triangle {(0,0),(1,0),(1,1)} if fx >= fy
+ * else {(0,0),(0,1),(1,1)}; barycentric weights. */
+void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]) {
+  float xs = x + 0.5f * y;
+  float fxs = floorf(xs), fys = floorf(y);
+  float fx = xs - fxs, fy = y - fys;
+  int64_t ix = (int64_t)fxs, iy = (int64_t)fys;
+  if (fx >= fy) {
+    lx[0] = ix;     ly[0] = iy;     beta[0] = 1.0f - fx;
+    lx[1] = ix + 1; ly[1] = iy;     beta[1] = fx - fy;
+    lx[2] = ix + 1; ly[2] = iy + 1; beta[2] = fy;
+  } else {
+    lx[0] = ix;     ly[0] = iy;     beta[0] = 1.0f - fy;
+    lx[1] = ix;     ly[1] = iy + 1; beta[1] = fy - fx;
+    lx[2] = ix + 1; ly[2] = iy + 1; beta[2] = fx;
+  }
+}
+
+/* ---------------------------------------------------------------------- */
+/* S6  Gated Gaussian binomial (Eq. 16-18, readings R-1..R-4):
+ * P>=1 = 1 - (1-p)^n; mu = (n-1)p, sigma = sqrt((n-1)p(1-p)); gate succeeds
+ * iff theta0 < P>=1 with theta0 = (h >> 9) 2^-23, i.e. (h >> 9) < T where
+ * T = ceil(P>=1 2^23); count = clamp(floor(1 + mu + sigma z), 1, ceil(n)).   */
+/* ---------------------------------------------------------------------- */
+void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap) {
+  if (!(n > 0.0f) || !(p > 0.0f)) { *T = 0; *sigma = 0.0f; *m1 = 1.0f; *cap = 1.0f; return; }
+  float Pge1;
+  if (p >= 1.0f) {
+    Pge1 = 1.0f;
+  } else {
+    float y = n * orc_log2_1mp(p);      /* log2((1-p)^n) */
+    Pge1 = 1.0f - orc_exp2(y);          /* Eq. 16 */
+  }
+  *T = (uint32_t)ceilf(Pge1 * 0x1p23f);
+  float nm1 = n - 1.0f;
+  float mu = nm1 > 0.0f ? nm1 * p : 0.0f; /* Eq. 17 (R-4: n < 1 -> mu = 0) */
+  *sigma = sqrtf(mu * (1.0f - p));
+  *m1 = 1.0f + mu;
+  *cap = ceilf(n);
+}
+
+int32_t orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap) {
+  orc_init();
+  if (!((h >> 9) < T)) return 0;                  /* H(P>=1 - theta0) gate, R-1 */
+  float z = g_z[h & (ORC_ZQ - 1)];                /* N(theta1) via quantile table, R-2 */
+  float x = fmaf(sigma, z, m1);                   /* 1 + N(theta1; mu, sigma) */
+  x = x < 1.0f ? 1.0f : x;                        /* R-3 clamp */
+  x = x > cap ? cap : x;
+  return (int32_t)floorf(x);                      /* Eq. 18 floor, R-26 */
+}
+
+/* exact test sampler (sampler = 1): Bin(floor n, p) + Bernoulli(frac(n) p),
+ * trials driven by the same per-draw hash; mean is exactly n p. fp64. */
+static int32_t exact_count(uint32_t h, float n, float p) {
+  if (!(n > 0.0f) || !(p > 0.0f)) return 0;
+  double dn = (double)n, dp = (double)p;
+  int64_t nf = (int64_t)floor(dn);
+  int32_t c = 0;
+  for (int64_t t = 0; t < nf; ++t) {
+    uint32_t u = orc_lowbias32(h ^ orc_lowbias32((uint32_t)t * 0x9e3779b9U + 0x632be5abU));
+    if ((double)u * 0x1p-32 < dp) ++c;
+  }
+  uint32_t u = orc_lowbias32(h ^ 0xa5a5a5a5U);
+  if ((double)u * 0x1p-32 < (dn - (double)nf) * dp) ++c;
+  return c;
+}
+
+/* ---------------------------------------------------------------------- */
+/* S5  NDF ratio D(h)/D(n) (Eq. 4; targets P:L148, L1211; anisotropic
+ * alpha reading R-22). GGX: 1/q^2, q = X^2+Y^2+hz^2; Beckmann:
+ * exp(-(X^2+Y^2)/hz^2)/hz^4; X = hx/ax, Y = hy/ay.                           */
+/* ---------------------------------------------------------------------- */
+float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz) {
+  if (!(hz > 0.0f)) return 0.0f;
+  float X = hx / ax, Y = hy / ay;
+  float s2 = X * X + Y * Y;
+  float hz2 = hz * hz;
+  if (ndf_kind == 0) {
+    float q = s2 + hz2;
+    return 1.0f / (q * q);
+  }
+  float e2 = s2 / hz2;
+  return orc_exp2(-(e2 * 0x1.715476p+0f)) / (hz2 * hz2);
+}
+
+/* fp32 contract vector helpers */
+static float dot3f(const float a[3], const float b[3]) {
+  return fmaf(a[2], b[2], fmaf(a[1], b[1], a[0] * b[0]));
+}
+static void normalize3f(float v[3]) {
+  float l2 = dot3f(v, v);
+  float inv = 1.0f / sqrtf(l2);
+  v[0] = v[0] * inv; v[1] = v[1] * inv; v[2] = v[2] * inv;
+}
+/* Duff et al. 2017 branchless ONB from n (reading R-17) */
+static void onb_f(const float n[3], float t[3], float bt[3]) {
+  float sgn = copysignf(1.0f, n[2]);
+  float a = -1.0f / (sgn + n[2]);
+  float b = (n[0] * n[1]) * a;
+  float nxxa = (n[0] * n[0]) * a;
+  float nyya = (n[1] * n[1]) * a;
+  t[0] = 1.0f + sgn * nxxa; t[1] = sgn * b; t[2] = -(sgn * n[0]);
+  bt[0] = b; bt[1] = sgn + nyya; bt[2] = -n[1];
+}
+
+/* fp64 radiance helpers (tolerance path; Eq. 1-2, reading R-21) */
+static double dot3d(const double a[3], const double b[3]) { return a[0]*b[0] + a[1]*b[1] + a[2]*b[2]; }
+static void normalize3d(double v[3]) { double l = sqrt(dot3d(v, v)); v[0] /= l; v[1] /= l; v[2] /= l; }
+static void onb_d(const double n[3], double t[3], double bt[3]) {
+  double sgn = n[2] >= 0.0 ? 1.0 : -1.0;
+  double a = -1.0 / (sgn + n[2]);
+  double b = n[0] * n[1] * a;
+  t[0] = 1.0 + sgn * n[0] * n[0] * a; t[1] = sgn * b; t[2] = -sgn * n[0];
+  bt[0] = b; bt[1] = sgn + n[1] * n[1] * a; bt[2] = -n[1];
+}
+/* Smith Lambda (height-correlated G2 = 1/(1 + L(wi) + L(wo))) */
+static double smith_lambda(int kind, double ax, double ay, const double wl[3]) {
+  double s = ax * ax * wl[0] * wl[0] + ay * ay * wl[1] * wl[1];
+  if (s <= 0.0) return 0.0;
+  if (kind == 0) { /* GGX, exact: (-1 + sqrt(1 + s/wz^2))/2, stable form */
+    double q = s / (wl[2] * wl[2]);
+    return q / (2.0 * (1.0 + sqrt(1.0 + q)));
+  }
+  double a = wl[2] / sqrt(s); /* Beckmann, Walter et al. 2007 rational fit */
+  if (a >= 1.6) return 0.0;
+  return (1.0 - 1.259 * a + 0.396 * a * a) / (3.535 * a + 2.181 * a * a);
+}
+
+/* radiance-path terms exported for pin tests (fp64; reading R-21):
+ * G2 = 1/(1 + Lambda(wi) + Lambda(wo)) in the local (t, b, n) frame, and
+ * Schlick F = f0 + (1 - f0)(1 - cos)^5. */
+double orc_smith_g2(int32_t kind, double ax, double ay, const double wi_l[3], const double wo_l[3]) {
+  return 1.0 / (1.0 + smith_lambda(kind, ax, ay, wi_l) + smith_lambda(kind, ax, ay, wo_l));
+}
+double orc_schlick(double f0, double cos_t) {
+  double om = 1.0 - cos_t;
+  return f0 + (1.0 - f0) * om * om * om * om * om;
+}
+
+/* ---------------------------------------------------------------------- */
+/* S0..S9 for one pixel                                                     */
+/* ---------------------------------------------------------------------- */
+static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4],
+                       const float pos[4], const float mat[4], const orc_scene* sc,
+                       double rgb[3], uint32_t* flags_out, orc_rec* rec) {
+  int L = sc->n_lights;
+  uint32_t flags = 0;
+  rgb[0] = rgb[1] = rgb[2] = 0.0;
+  if (rec) memset(rec, 0, sizeof(orc_rec) * (size_t)L);
+
+  uint32_t meta = f2u(uvm[3]);
+  float u = uvm[0], v = uvm[1];
+  if (!(meta & 1u)) { *flags_out = ORC_FLAG_INVALID; goto fill_flags; }
+  if (!(fabsf(u) <= 0x1p24f && fabsf(v) <= 0x1p24f)) {
+    *flags_out = ORC_FLAG_INVALID | ORC_FLAG_UV_RANGE; goto fill_flags;
+  }
+
+  /* S1 footprint */
+  float P, r, psi;
+  if (!orc_footprint(duv, &P, &r, &psi)) { *flags_out = ORC_FLAG_DEGENERATE; goto fill_flags; }
+
+  /* S2 lattice: 4 grids + distribution weights; n_i = w_i N 2^ls_i (R-14:
+   * "N_i proportional to its area") */
+  int32_t ls[4], lr[4], jo[4];
+  float w[4], n[4];
+  orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
+  float N = mat[2], R = mat[3], ax = mat[0], ay = mat[1];
+  for (int i = 0; i < 4; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
+
+  /* S3 + S4a: per grid, 3 simplex lattice vertices and their spatial seeds */
+  uint32_t obj = f2u(uvm[2]);
+  uint32_t so = orc_lowbias32(obj ^ orc_lowbias32(sc->seed));
+  uint32_t hs[4][3];
+  int64_t lxs[4][3], lys[4][3];
+  double betad[4][3];
+  for (int i = 0; i < 4; ++i) {
+    float x, y, be[3];
+    orc_grid_uv(u, v, ls[i], lr[i], jo[i], &x, &y);
+    orc_simplex(x, y, lxs[i], lys[i], be);
+    /* barycentrics recomputed in fp64 from the exact fp32 fractions */
+    {
+      float xs = x + 0.5f * y;
+      double fx = (double)(xs - floorf(xs)), fy = (double)(y - floorf(y));
+      if (fx >= fy) { betad[i][0] = 1.0 - fx; betad[i][1] = fx - fy; betad[i][2] = fy; }
+      else          { betad[i][0] = 1.0 - fy; betad[i][1] = fy - fx; betad[i][2] = fx; }
+    }
+    uint32_t gk = ((uint32_t)ls[i] & 511u) | ((uint32_t)lr[i] << 9) | ((uint32_t)jo[i] << 13);
+    uint32_t g = orc_lowbias32(so ^ gk);
+    for (int k = 0; k < 3; ++k) {
+      uint32_t lin = (uint32_t)lxs[i][k] * 0x8da6b343U + (uint32_t)lys[i][k] * 0xd8163841U;
+      hs[i][k] = orc_lowbias32(g ^ lin);
+    }
+  }
+
+  /* shading frame (fp32 contract; decides light activity, p, angular nodes) */
+  float nf[3] = {nrm[0], nrm[1], nrm[2]};
+  normalize3f(nf);
+  float tf[3], bf[3];
+  onb_f(nf, tf, bf);
+  float wi[3];
+  if (sc->view_kind == 0) { wi[0] = sc->view[0] - pos[0]; wi[1] = sc->view[1] - pos[1]; wi[2] = sc->view[2] - pos[2]; }
+  else { wi[0] = sc->view[0]; wi[1] = sc->view[1]; wi[2] = sc->view[2]; }
+  normalize3f(wi);
+  float ni = dot3f(nf, wi);
+  float inv_beta = 1.0f / sc->beta;
+
+  /* fp64 frame for radiance */
+  double nd[3] = {nrm[0], nrm[1], nrm[2]};
+  normalize3d(nd);
+  double td[3], bd[3];
+  onb_d(nd, td, bd);
+  double wid[3];
+  if (sc->view_kind == 0) { wid[0] = (double)sc->view[0] - pos[0]; wid[1] = (double)sc->view[1] - pos[1]; wid[2] = (double)sc->view[2] - pos[2]; }
+  else { wid[0] = sc->view[0]; wid[1] = sc->view[1]; wid[2] = sc->view[2]; }
+  normalize3d(wid);
+
+  for (int l = 0; l < L; ++l) {
+    const orc_light* lt = &sc->lights[l];
+    orc_rec* rc = rec ? &rec[l] : 0;
+    if (rc) {
+      rc->P = P; rc->r = r; rc->psi = psi;
+      for (int i = 0; i < 4; ++i) { rc->ls[i] = ls[i]; rc->lr[i] = lr[i]; rc->jo[i] = jo[i]; rc->w[i] = w[i]; rc->n[i] = n[i]; }
+      for (int i = 0; i < 4; ++i) for (int k = 0; k < 3; ++k) { rc->lx[i*3+k] = (int32_t)(uint32_t)lxs[i][k]; rc->ly[i*3+k] = (int32_t)(uint32_t)lys[i][k]; }
+    }
+    /* S5: light direction (P:L1228 punctual lights only, reading R-27) */
+    float wo[3];
+    if (lt->kind == 0) { wo[0] = lt->pos_or_dir[0] - pos[0]; wo[1] = lt->pos_or_dir[1] - pos[1]; wo[2] = lt->pos_or_dir[2] - pos[2]; }
+    else { wo[0] = lt->pos_or_dir[0]; wo[1] = lt->pos_or_dir[1]; wo[2] = lt->pos_or_dir[2]; }
+    normalize3f(wo);
+    float no = dot3f(nf, wo);
+    if (!(ni > 0.0f && no > 0.0f)) continue; /* light below the horizon: 0 */
+    if (rc) rc->light_active = 1;
+    float hv[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+    normalize3f(hv);
+    float hx = dot3f(hv, tf), hy = dot3f(hv, bf), hz = dot3f(hv, nf);
+    /* Eq. 4: p = R D(h)/D(n), clamped to 1 (reading R-19) */
+    float p = R * orc_ratio(sc->ndf_kind, ax, ay, hx, hy, hz);
+    if (p > 1.0f) { p = 1.0f; flags |= ORC_FLAG_P_CLAMPED; }
+    if (!(p > 0.0f)) p = 0.0f;
+    /* Eq. 14 angular grid: orthographic projection of h, cell size beta (R-17) */
+    float gx = fmaf(hx, inv_beta, -0.5f), gy = fmaf(hy, inv_beta, -0.5f);
+    float cxf = floorf(gx), cyf = floorf(gy);
+    double fxa = (double)(gx - cxf), fya = (double)(gy - cyf);
+    int32_t cx0 = (int32_t)cxf, cy0 = (int32_t)cyf;
+    double vj[4] = {(1.0 - fxa) * (1.0 - fya), fxa * (1.0 - fya), (1.0 - fxa) * fya, fxa * fya};
+    uint32_t ka[4];
+    for (int jn = 0; jn < 4; ++jn) {
+      uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
+      ka[jn] = orc_lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
+    }
+    if (rc) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
+
+    /* S6 + S7 + S8: 4 grids x 3 spatial x 4 angular = 48 draws */
+    double C = 0.0;
+    for (int i = 0; i < 4; ++i) {
+      uint32_t T; float sig, m1, cap;
+      orc_gate_params(n[i], p, &T, &sig, &m1, &cap);
+      if (rc) { rc->T[i] = T; rc->sigma[i] = sig; rc->m1[i] = m1; rc->cap[i] = cap; }
+      double Ci = 0.0; /* b_theta_i(w_i N_i, p), interpolated (Eq. 14, R-16) */
+      for (int k = 0; k < 3; ++k) {
+        double Cik = 0.0;
+        for (int jn = 0; jn < 4; ++jn) {
+          uint32_t h = orc_lowbias32(hs[i][k] ^ ka[jn]);
+          int32_t c = sc->sampler == 1 ? exact_count(h, n[i], p) : orc_gated_count(h, T, sig, m1, cap);
+          if (rc) { rc->hash[i*12 + k*4 + jn] = h; rc->count[i*12 + k*4 + jn] = c; }
+          Cik += vj[jn] * (double)c;
+        }
+        Ci += betad[i][k] * Cik;
+      }
+      C += Ci; /* distributed law: sum over the 4 grids (Eq. 10/13) */
+    }
+
+    /* S8: Eq. 3-4, D_P = D(n)/R * b / N(P), N(P) = N P (reading R-20) */
+    double Dn = 1.0 / (M_PI * (double)ax * (double)ay);
+    double Dp = Dn * C / ((double)R * (double)N * (double)P);
+
+    /* S9: Eq. 1-2 with a punctual light: L += F G D_P E / (4 n.wi) */
+    double wod[3];
+    double E[3];
+    if (lt->kind == 0) {
+      wod[0] = (double)lt->pos_or_dir[0] - pos[0]; wod[1] = (double)lt->pos_or_dir[1] - pos[1]; wod[2] = (double)lt->pos_or_dir[2] - pos[2];
+      double d2 = dot3d(wod, wod);
+      for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch] / d2;
+    } else {
+      wod[0] = lt->pos_or_dir[0]; wod[1] = lt->pos_or_dir[1]; wod[2] = lt->pos_or_dir[2];
+      for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch];
+    }
+    normalize3d(wod);
+    double hd[3] = {wid[0] + wod[0], wid[1] + wod[1], wid[2] + wod[2]};
+    normalize3d(hd);
+    double nid = dot3d(nd, wid);
+    double cih = dot3d(wid, hd);
+    double wil[3] = {dot3d(wid, td), dot3d(wid, bd), nid};
+    double wol[3] = {dot3d(wod, td), dot3d(wod, bd), dot3d(wod, nd)};
+    double G2 = 1.0 / (1.0 + smith_lambda(sc->ndf_kind, ax, ay, wil) + smith_lambda(sc->ndf_kind, ax, ay, wol));
+    for (int ch = 0; ch < 3; ++ch) {
+      double F = orc_schlick((double)sc->f0[ch], cih);
+      rgb[ch] += F * G2 * Dp * E[ch] / (4.0 * nid);
+    }
+    if (rc) { rc->C = (float)C; rc->Dp = (float)Dp; }
+  }
+  *flags_out = flags;
+fill_flags:
+  if (rec) for (int l = 0; l < L; ++l) rec[l].flags = *flags_out;
+}
+
+int orc_eval(const float* duv, const float* uvm, const float* nrm, const float* pos,
+             const float* mat, int64_t n, const orc_scene* sc, double* rgb,
+             uint32_t* flags, orc_rec* rec) {
+  orc_init();
+  if (sc->n_lights < 0 || sc->n_lights > ORC_MAX_LIGHTS) return -1;
+  for (int64_t i = 0; i < n; ++i)
+    eval_pixel(duv + 4 * i, uvm + 4 * i, nrm + 4 * i, pos + 4 * i, mat + 4 * i, sc,
+               rgb + 3 * i, flags + i, rec ? rec + i * sc->n_lights : 0);
+  return 0;
+}

@@ -1,0 +1,77 @@
+"""Pins for the NDF ratio (Eq. 4; targets P:L148, L1211), the BRDF
+shell (Eq. 1-2; readings R-21, R-22) against quadrature, textbook
+closed forms and reciprocity."""
+import math
+
+import numpy as np
+import pytest
+from scipy import integrate
+
+from oracle import stats
+
+
+@pytest.mark.parametrize("ndf", ["ggx", "beckmann"])
+@pytest.mark.parametrize("ax,ay", [(0.3, 0.3), (1.0, 1.0), (0.2, 0.5)])
+def test_ndf_projected_area_normalisation(orc, ndf, ax, ay):
+    """int D(h) cos(theta_h) dw = 1 with D = D(n) * ratio(h), D(n) = 1/(pi ax ay)."""
+    Dn = 1.0 / (math.pi * ax * ay)
+
+    def f(th, ph):
+        h = (math.sin(th) * math.cos(ph), math.sin(th) * math.sin(ph), math.cos(th))
+        return Dn * orc.ratio(ndf, ax, ay, *h) * math.cos(th) * math.sin(th)
+
+    val, _ = integrate.dblquad(lambda th, ph: f(th, ph), 0, 2 * math.pi, 0, math.pi / 2,
+                               epsabs=1e-5, epsrel=1e-5)
+    assert abs(val - 1.0) < 5e-3, val
+
+
+def test_ratio_closed_forms(orc):
+    assert abs(orc.ratio("ggx", 0.3, 0.3, 0.0, 0.0, 1.0) - 1.0) < 1e-6      # h = n -> 1
+    assert abs(orc.ratio("beckmann", 0.3, 0.3, 0.0, 0.0, 1.0) - 1.0) < 1e-6
+    s = math.sqrt(0.5)                                                         # Beckmann a=1, 45 deg: 4/e
+    assert abs(orc.ratio("beckmann", 1.0, 1.0, s, 0.0, s) - 4 / math.e) < 2e-6
+    h = np.array([0.3, -0.2, math.sqrt(1 - 0.13)])
+    for ndf in ("ggx", "beckmann"):
+        ref = stats.ndf_D(ndf, 0.25, 0.4, h) * math.pi * 0.25 * 0.4
+        assert abs(orc.ratio(ndf, 0.25, 0.4, *h) - ref) < 2e-6 * max(1, ref)
+    assert orc.ratio("ggx", 0.3, 0.3, 1.0, 0.0, 0.0) == 0.0                    # grazing h
+
+
+def test_schlick():
+    import oracle
+    assert abs(oracle.schlick(0.04, 0.5) - 0.07) < 1e-15
+    assert oracle.schlick(0.3, 1.0) == 0.3 and oracle.schlick(0.3, 0.0) == 1.0
+
+
+@pytest.mark.parametrize("ndf", ["ggx", "beckmann"])
+def test_smith_g1_vs_exact_lambda(orc, ndf):
+    """With wo = n (Lambda = 0), G2 = G1(wi) = 1/(1 + Lambda(wi)); GGX exact,
+    Beckmann's rational fit within 0.5 % of the erf form."""
+    for alpha in (0.1, 0.3, 0.7, 1.0):
+        for th in np.linspace(0.05, 1.5, 20):
+            wi = (math.sin(th), 0.0, math.cos(th))
+            g = orc.smith_g2(ndf, alpha, alpha, wi, (0.0, 0.0, 1.0))
+            ref = 1.0 / (1.0 + stats.smith_lambda_exact(ndf, alpha, math.cos(th)))
+            assert abs(g - ref) < (1e-12 if ndf == "ggx" else 5e-3 * ref)
+
+
+@pytest.mark.parametrize("ndf", ["ggx", "beckmann"])
+def test_reciprocity_of_the_glint_brdf(orc, ndf):
+    """rho = F G D_P / (4 (n.wi)(n.wo)) is symmetric: h, hence every count, is
+    unchanged when view and light swap, so rgb * (n.wi) is symmetric too."""
+    from paper_2306_05051_b200 import synth
+    rng = np.random.default_rng(7)
+    for _ in range(6):
+        a = rng.standard_normal(3); a[2] = abs(a[2]) + 0.2; a /= np.linalg.norm(a)
+        b = rng.standard_normal(3); b[2] = abs(b[2]) + 0.2; b /= np.linalg.norm(b)
+        a, b = a.astype(np.float32).astype(float), b.astype(np.float32).astype(float)
+        fr = synth.c1(ndf, "mirror")
+        fr.scene.lights[0] = synth.Light("directional", tuple(b), (1.0, 1.0, 1.0))
+        fr.scene.view = tuple(a)
+        rgb1, _, rec1 = orc.eval(fr.gbuf, fr.scene, debug=True)
+        fr.scene.lights[0] = synth.Light("directional", tuple(a), (1.0, 1.0, 1.0))
+        fr.scene.view = tuple(b)
+        rgb2, _, rec2 = orc.eval(fr.gbuf, fr.scene, debug=True)
+        assert np.array_equal(rec1["count"], rec2["count"])
+        na, nb = a[2] / np.linalg.norm(a), b[2] / np.linalg.norm(b)
+        assert np.allclose(rgb1 * na, rgb2 * nb, rtol=1e-9, atol=0)

@@ -1,0 +1,110 @@
+"""Pins for the oracle's fp32 contract functions against libm /
+scipy in fp64 -- i.e. against the mathematics, not against themselves."""
+import math
+
+import numpy as np
+import pytest
+from scipy import special
+
+
+def f32(x):
+    return float(np.float32(x))
+
+
+def test_exp2_matches_libm(orc):
+    ys = np.concatenate([-np.linspace(0, 125, 20001), -np.geomspace(1e-12, 1, 2001)])
+    worst = 0.0
+    for y in ys.astype(np.float32):
+        got = orc.exp2(float(y))
+        ref = 2.0 ** float(y)
+        worst = max(worst, abs(got - ref) / ref)
+    assert worst < 4e-7, worst
+    # exact anchors: 2^0 = 1, 2^-1 = 1/2, 2^-k exact, below -125 -> 0 (contract)
+    assert orc.exp2(0.0) == 1.0 and orc.exp2(-1.0) == 0.5 and orc.exp2(-20.0) == 2.0 ** -20
+    assert orc.exp2(-126.0) == 0.0 and orc.exp2(-1e30) == 0.0
+
+
+def test_log2_1mp_matches_libm(orc):
+    ps = np.concatenate([np.geomspace(1e-38, 0.5, 3001), np.linspace(0.5, 1 - 1e-7, 3001)]).astype(np.float32)
+    worst = 0.0
+    for p in ps:
+        p = float(p)
+        if not (0.0 < p < 1.0):
+            continue
+        ref = math.log1p(-p) / math.log(2.0)
+        got = orc.log2_1mp(p)
+        worst = max(worst, abs(got - ref) / abs(ref))
+    assert worst < 4e-7, worst
+    assert orc.log2_1mp(0.5) == -1.0 and orc.log2_1mp(0.75) == -2.0
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_atan2_turns_matches_libm(orc, seed):
+    rng = np.random.default_rng(seed)
+    y = rng.standard_normal(20000) * np.exp(rng.uniform(-20, 20, 20000))
+    x = rng.standard_normal(20000) * np.exp(rng.uniform(-20, 20, 20000))
+    worst = 0.0
+    for yy, xx in zip(y.astype(np.float32), x.astype(np.float32)):
+        got = orc.atan2_turns(float(yy), float(xx))
+        ref = math.atan2(float(yy), float(xx)) / (2 * math.pi)
+        worst = max(worst, abs(got - ref))
+    assert worst < 2e-7, worst
+
+
+def test_atan2_turns_special_cases(orc):
+    # axes and diagonals are exact in turns (quadrant fix-ups are exact)
+    assert orc.atan2_turns(0.0, 1.0) == 0.0
+    assert orc.atan2_turns(1.0, 0.0) == 0.25
+    assert orc.atan2_turns(0.0, -1.0) == 0.5
+    assert orc.atan2_turns(-1.0, 0.0) == -0.25
+    assert orc.atan2_turns(0.0, 0.0) == 0.0
+    assert abs(orc.atan2_turns(1.0, 1.0) - 0.125) < 1e-8
+    assert abs(orc.atan2_turns(-3.0, -3.0) + 0.375) < 1e-8
+
+
+def test_lowbias32_is_a_bijection_and_avalanches(orc):
+    """lowbias32 = xorshift16, *odd, xorshift15, *odd, xorshift16: each step is
+    invertible, so inverting it step by step must round-trip; flipping one input
+    bit flips ~16 output bits on average."""
+    inv = lambda a: pow(a, -1, 1 << 32)
+
+    def unxorshift(x, s):
+        y = x
+        for _ in range(32 // s + 1):
+            y = x ^ (y >> s)
+        return y & 0xFFFFFFFF
+
+    def inverse(h):
+        h = unxorshift(h, 16)
+        h = (h * inv(0x846CA68B)) & 0xFFFFFFFF
+        h = unxorshift(h, 15)
+        h = (h * inv(0x7FEB352D)) & 0xFFFFFFFF
+        return unxorshift(h, 16)
+
+    rng = np.random.default_rng(3)
+    xs = rng.integers(0, 2 ** 32, 2000, dtype=np.uint64)
+    flips = []
+    for x in xs:
+        x = int(x)
+        h = orc.lowbias32(x)
+        assert inverse(h) == x
+        for b in range(0, 32, 4):
+            flips.append(bin(h ^ orc.lowbias32(x ^ (1 << b))).count("1"))
+    assert 15.5 < np.mean(flips) < 16.5
+
+
+def test_z_table_is_the_gaussian_quantile(orc):
+    """Z[k] = fp32(Phi^-1((k+1/2)/4096)) bit-for-bit vs scipy's ndtri (reading R-2)."""
+    z = orc.ztable()
+    ref = special.ndtri((np.arange(4096) + 0.5) / 4096.0).astype(np.float32)
+    assert np.array_equal(z.view(np.uint32), ref.view(np.uint32))
+    # symmetry and the moments quoted in SURVEY Appendix A (min z -3.668, Var 0.99968)
+    assert np.array_equal(z, -z[::-1])
+    assert abs(float(z.min()) + 3.668) < 1e-3
+    assert abs(float(np.var(z.astype(np.float64))) - 0.99968) < 2e-5
+
+
+def test_orientation_table(orc):
+    m = np.arange(256)
+    assert np.array_equal(orc.costable(), np.cos(m * np.pi / 256).astype(np.float32))
+    assert np.array_equal(orc.sintable(), np.sin(m * np.pi / 256).astype(np.float32))
