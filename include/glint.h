@@ -1,0 +1,175 @@
+/*
+ * glint.h -- C ABI of the B200-native glint evaluation library (libglint.so).
+ *
+ * Implements the per-pixel glinty-BRDF evaluation of arXiv 2306.05051
+ * ("distributed binomial laws on anisotropic grids") for a structure-of-arrays
+ * G-buffer on NVIDIA B200 (sm_100a). One call = one kernel launch that runs
+ * every step of the path for every (pixel, light):
+ *
+ *   S1 footprint from screen-space uv derivatives
+ *   S2 anisotropic lattice: scale (Eq. 13), ratio/orientation
+ *      (Fig. 6), 9-tetrahedra cell split -> 4 grids
+ *   S3 grid transform (Eq. 12) + simplex surface grid
+ *   S4 per-texel seeds coherent across LODs
+ *   S5 p = R D(h)/D(n) (Eq. 4) + angular grid (Eq. 14)
+ *   S6/S7 48 gated Gaussian binomial draws (Eq. 16-18)
+ *   S8 distributed law + interpolation -> D_P (Eq. 3, 10)
+ *   S9 microfacet radiance (Eq. 1-2), punctual lights
+ *
+ * P:Lnnn = line of the paper's text. The exact fp32 arithmetic of
+ * every step is the contract of DESIGN.md §4; where the paper is silent the
+ * readings of DESIGN.md §5 apply.
+ *
+ * Conventions
+ *  - All functions return GLINT_OK (0) or a negative GLINT_E* code; no
+ *    exception crosses the ABI. glint_strerror() describes a code.
+ *  - Device pointers are CUDA device addresses on the context's device; the
+ *    caller owns every buffer (typically torch tensors). The library never
+ *    allocates or frees caller memory and never synchronises the stream in
+ *    glint_eval (errors of asynchronous execution surface at the caller's
+ *    next synchronisation).
+ *  - cudaStream_t is passed as void* (NULL = legacy default stream).
+ */
+#ifndef GLINT_H
+#define GLINT_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLINT_VERSION 10000 /* 1.0.0 */
+
+/* return codes */
+#define GLINT_OK 0
+#define GLINT_EINVAL -1   /* null pointer, size <= 0, bad enum, K not in [1,8], beta <= 0, n_lights not in [0,16] */
+#define GLINT_EALIGN -2   /* a plane / output pointer not 16-byte aligned, pitch < width */
+#define GLINT_EDEVICE -3  /* no CUDA device, device is not sm_100, or ctx/device mismatch */
+#define GLINT_ELIMIT -4   /* width*height or pitch*height >= 2^31 pixels */
+#define GLINT_ECUDA -5    /* a CUDA runtime call failed; see glint_last_cuda_error() */
+#define GLINT_ENOMEM -6   /* host or device allocation failed */
+
+/* per-pixel output flags, stored as the bit pattern of out[pixel].w */
+#define GLINT_FLAG_INVALID 1u        /* meta bit0 clear: pixel not shaded */
+#define GLINT_FLAG_DEGENERATE 2u     /* |det J| outside [2^-64, 2^64) or non-finite */
+#define GLINT_FLAG_RATIO_CLAMPED 4u  /* anisotropy r > 2^K, clamped (reading R-25) */
+#define GLINT_FLAG_P_CLAMPED 8u      /* R D(h)/D(n) > 1 for some light, clamped (R-19) */
+#define GLINT_FLAG_UV_RANGE 16u      /* |u| or |v| > 2^24 (uv must be tile-local); with INVALID */
+
+#define GLINT_MAX_LIGHTS 16
+#define GLINT_ZQ 4096     /* quantile table size (reading R-2) */
+#define GLINT_NANG 256    /* orientation table size: phi_m = m pi / 256 */
+
+typedef struct glint_ctx glint_ctx;
+
+/* A punctual light. kind 0 = point at pos_or_dir (E = I / d^2),
+ * kind 1 = directional, pos_or_dir points toward the light (E = I). */
+typedef struct {
+  int32_t kind;
+  float pos_or_dir[3];
+  float intensity[3];   /* RGB */
+  int32_t reserved;
+} glint_light;
+
+/* Scene constants, passed BY VALUE to the kernel (lands in the launch's
+ * constant bank; concurrent evals on different streams cannot race). */
+typedef struct {
+  uint32_t seed;            /* hash seed (reading R-23) */
+  int32_t ndf_kind;         /* 0 = GGX, 1 = Beckmann */
+  int32_t max_ratio_level;  /* K in [1, 8]: anisotropy levels r = 2^0..2^K (R-9) */
+  float beta;               /* angular cell size / micro-roughness, > 0 (R-17) */
+  float f0[3];              /* Schlick F0, RGB (R-21) */
+  int32_t view_kind;        /* 0 = pinhole camera at view[], 1 = directional view[] */
+  float view[3];
+  int32_t n_lights;         /* 0 .. GLINT_MAX_LIGHTS */
+  int32_t reserved[4];
+  glint_light lights[GLINT_MAX_LIGHTS];
+} glint_scene;
+
+/* Structure-of-arrays G-buffer. Five planes of float4 per pixel, row-major,
+ * `pitch` float4 elements between rows (pitch >= width), 16-byte aligned:
+ *   duv = (du/dx, dv/dx, du/dy, dv/dy)  screen-space uv derivatives
+ *   uvm = (u, v, obj, meta)             tile-local uv; obj and meta are uint32
+ *                                       bit patterns; meta bit0 = pixel valid
+ *   nrm = (nx, ny, nz, -)               shading normal (normalised in-kernel)
+ *   pos = (x, y, z, -)                  world position (point lights / camera)
+ *   mat = (alpha_x, alpha_y, N, R)      roughness, flakes per unit uv^2, glint ratio R
+ * For glint_eval the planes are device pointers; for glint_eval_host they are
+ * host pointers (pinned memory gives full PCIe/C2C bandwidth). */
+typedef struct {
+  const void* duv;
+  const void* uvm;
+  const void* nrm;
+  const void* pos;
+  const void* mat;
+  int32_t width;
+  int32_t height;
+  int64_t pitch;
+} glint_gbuffer;
+
+/* Optional per (pixel, light) debug record (168 words, 672 bytes), written
+ * in-kernel by the same arithmetic (template instantiation) when `dbg` is
+ * non-NULL; record index = (y * width + x) * n_lights + light. For tiny
+ * parity inputs only. Fields mirror DESIGN.md §4.3. */
+typedef struct {
+  float P, r, psi;                 /* S1 footprint */
+  int32_t ls[4], lr[4], jo[4];     /* S2 grid vertices (log2 texel area, ratio level, orientation) */
+  float w[4], n[4];                /* distribution weights, trial counts n_i = w_i N 2^ls_i */
+  int32_t lx[12], ly[12];          /* S3 simplex lattice vertices (low 32 bits), slot-major */
+  float p;                         /* S5 success probability */
+  int32_t cx0, cy0;                /* S5 angular base node */
+  uint32_t T[4];                   /* S6 gate thresholds ceil(P>=1 2^23) */
+  float sigma[4], m1[4], cap[4];   /* S6 Gaussian parameters */
+  uint32_t hash[48];               /* S7 draw hashes, index = slot*12 + texel*4 + node */
+  float count[48];                 /* S7 flake counts (integer-valued fp32; may exceed 2^31) */
+  float C;                         /* S8 blended count */
+  float Dp;                        /* S8 D_P(h) */
+  uint32_t flags;
+  uint32_t light_active;           /* n.wi > 0 and n.wo > 0 */
+  uint32_t reserved[2];
+} glint_debug_rec;
+
+int glint_version(void);
+const char* glint_strerror(int code);
+/* CUDA error code (cudaError_t value) of the most recent GLINT_ECUDA in this thread. */
+int glint_last_cuda_error(void);
+
+/* Host-only: build the tables exactly as glint_create uploads them:
+ * z[k] = fp32(Phi^-1((k + 1/2) / 4096)), cosv[m] = fp32(cos(m pi/256)),
+ * sinv[m] = fp32(sin(m pi/256)); computed in double precision. Any pointer may
+ * be NULL. Needs no GPU. */
+int glint_build_tables(float* z, float* cosv, float* sinv);
+
+/* Create a context on `device` (must be sm_100): builds and uploads the
+ * tables ("precompute once at startup"). The context is immutable
+ * after creation; glint_eval may be called concurrently on different streams.
+ * Returns GLINT_EDEVICE if no sm_100 device is present. */
+int glint_create(glint_ctx** out, int device);
+int glint_destroy(glint_ctx* ctx);
+
+/* Evaluate every pixel of `gb` (device planes) for every light of `scene`:
+ * out[y * out_pitch + x] = float4(R, G, B, flags bits) for all pixels (fully
+ * overwritten). `dbg` (device, nullable) receives width*height*n_lights
+ * records. One kernel launch on `stream`; asynchronous. */
+int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
+               void* out, int64_t out_pitch, glint_debug_rec* dbg, void* stream);
+
+/* End-to-end entry with HOST buffers: copies the planes host->device, runs the
+ * kernel and copies the radiance device->host, pipelined over row chunks on
+ * two internal streams (copy/compute overlap). Uses device staging owned by
+ * the context (grown on demand, freed by glint_destroy); NOT reentrant on one
+ * context. Synchronous: returns after `out` (host, out_pitch float4 per row)
+ * is complete. `stream` orders the work after the caller's prior work. */
+int glint_eval_host(glint_ctx* ctx, const glint_gbuffer* gb_host, const glint_scene* scene,
+                    void* out_host, int64_t out_pitch, void* stream);
+
+/* Copies of the device-resident tables (host pointers), for parity tests. */
+int glint_get_tables(const glint_ctx* ctx, float* z, float* cosv, float* sinv);
+
+/* Number of kernel launches issued by this context so far (bench evidence). */
+int64_t glint_launch_count(const glint_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLINT_H */

@@ -62,7 +62,7 @@ REC_DTYPE = np.dtype([
     ("lx", "<i4", 12), ("ly", "<i4", 12),
     ("p", "<f4"), ("cx0", "<i4"), ("cy0", "<i4"),
     ("T", "<u4", 4), ("sigma", "<f4", 4), ("m1", "<f4", 4), ("cap", "<f4", 4),
-    ("hash", "<u4", 48), ("count", "<i4", 48),
+    ("hash", "<u4", 48), ("count", "<f4", 48),
     ("C", "<f4"), ("Dp", "<f4"), ("flags", "<u4"), ("light_active", "<u4"), ("pad_", "<u4", 2),
 ])
 assert REC_DTYPE.itemsize == 168 * 4
@@ -99,7 +99,7 @@ def lib():
             L.orc_gate_params.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_uint32), fp, fp, fp]
             L.orc_gate_params.restype = None
             L.orc_gated_count.argtypes = [C.c_uint32, C.c_uint32, C.c_float, C.c_float, C.c_float]
-            L.orc_gated_count.restype = C.c_int32
+            L.orc_gated_count.restype = C.c_float
             L.orc_ratio.argtypes = [C.c_int32] + [C.c_float] * 5
             L.orc_ratio.restype = C.c_float
             d3 = C.c_double * 3
@@ -245,7 +245,7 @@ def gate_params(n: float, p: float):
 
 
 def gated_count(h: int, T: int, sigma: float, m1: float, cap: float) -> int:
-    return lib().orc_gated_count(h & 0xFFFFFFFF, T, sigma, m1, cap)
+    return int(lib().orc_gated_count(h & 0xFFFFFFFF, T, sigma, m1, cap))
 
 
 def ratio(ndf: str, ax, ay, hx, hy, hz) -> float:

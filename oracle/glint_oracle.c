@@ -352,20 +352,20 @@ void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, flo
   *cap = ceilf(n);
 }
 
-int32_t orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap) {
+float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap) {
   orc_init();
-  if (!((h >> 9) < T)) return 0;                  /* H(P>=1 - theta0) gate, R-1 */
+  if (!((h >> 9) < T)) return 0.0f;               /* H(P>=1 - theta0) gate, R-1 */
   float z = g_z[h & (ORC_ZQ - 1)];                /* N(theta1) via quantile table, R-2 */
   float x = fmaf(sigma, z, m1);                   /* 1 + N(theta1; mu, sigma) */
   x = x < 1.0f ? 1.0f : x;                        /* R-3 clamp */
   x = x > cap ? cap : x;
-  return (int32_t)floorf(x);                      /* Eq. 18 floor, R-26 */
+  return floorf(x);                               /* Eq. 18 floor, R-26 */
 }
 
 /* exact test sampler (sampler = 1): Bin(floor n, p) + Bernoulli(frac(n) p),
  * trials driven by the same per-draw hash; mean is exactly n p. fp64. */
-static int32_t exact_count(uint32_t h, float n, float p) {
-  if (!(n > 0.0f) || !(p > 0.0f)) return 0;
+static float exact_count(uint32_t h, float n, float p) {
+  if (!(n > 0.0f) || !(p > 0.0f)) return 0.0f;
   double dn = (double)n, dp = (double)p;
   int64_t nf = (int64_t)floor(dn);
   int32_t c = 0;
@@ -375,7 +375,7 @@ static int32_t exact_count(uint32_t h, float n, float p) {
   }
   uint32_t u = orc_lowbias32(h ^ 0xa5a5a5a5U);
   if ((double)u * 0x1p-32 < (dn - (double)nf) * dp) ++c;
-  return c;
+  return (float)c;
 }
 
 /* ---------------------------------------------------------------------- */
@@ -574,7 +574,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
         double Cik = 0.0;
         for (int jn = 0; jn < 4; ++jn) {
           uint32_t h = orc_lowbias32(hs[i][k] ^ ka[jn]);
-          int32_t c = sc->sampler == 1 ? exact_count(h, n[i], p) : orc_gated_count(h, T, sig, m1, cap);
+          float c = sc->sampler == 1 ? exact_count(h, n[i], p) : orc_gated_count(h, T, sig, m1, cap);
           if (rc) { rc->hash[i*12 + k*4 + jn] = h; rc->count[i*12 + k*4 + jn] = c; }
           Cik += vj[jn] * (double)c;
         }

@@ -60,7 +60,7 @@ typedef struct {
   uint32_t T[4];                   /* gate thresholds, ceil(P>=1 * 2^23) */
   float sigma[4], m1[4], cap[4];   /* Eq. 17 parameters */
   uint32_t hash[48];               /* per-draw 32-bit hash */
-  int32_t count[48];               /* per-draw flake count */
+  float count[48];                 /* per-draw flake count (integer-valued fp32) */
   float C;                         /* blended count (fp32 view of the fp64 value) */
   float Dp;                        /* D_P(h) (Eq. 3), fp32 view */
   uint32_t flags;
@@ -90,7 +90,7 @@ int orc_lattice(float P, float r, float psi, int32_t K, int32_t ls[4], int32_t l
 void orc_grid_uv(float u, float v, int32_t ls, int32_t lr, int32_t jo, float* x, float* y);
 void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]);
 void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap);
-int32_t orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap);
+float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap);
 float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz);
 double orc_smith_g2(int32_t kind, double ax, double ay, const double wi_l[3], const double wo_l[3]);
 double orc_schlick(double f0, double cos_t);

@@ -1,0 +1,336 @@
+// glint_api.cu -- host side of the C ABI declared in include/glint.h.
+//
+// Validation, table construction (double precision on the host, rounded to
+// fp32: "a small texture of random numbers that we precompute once at
+// startup"), launch-shape selection and the end-to-end host-buffer pipeline.
+// No arithmetic of the glint path runs here.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "../../include/glint.h"
+#include "glint_kernel.h"
+
+static thread_local int g_last_cuda = 0;
+
+#define GL_CUDA(call)                                \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) {                         \
+      g_last_cuda = (int)e_;                         \
+      return GLINT_ECUDA;                            \
+    }                                                \
+  } while (0)
+
+struct glint_ctx {
+  int device;
+  int sm_count;
+  int blocks_per_sm;
+  float* d_z;
+  float2* d_cs;
+  float h_z[GLINT_ZQ];
+  float h_cos[GLINT_NANG], h_sin[GLINT_NANG];
+  std::atomic<int64_t> launches;
+  // glint_eval_host staging (2 buffers x (5 planes + out)), grown on demand
+  size_t stage_px;
+  float4* d_stage[2][6];
+  cudaStream_t st[2];
+  cudaEvent_t ev_in, ev_done[2];
+};
+
+extern "C" int glint_version(void) { return GLINT_VERSION; }
+
+extern "C" const char* glint_strerror(int code) {
+  switch (code) {
+    case GLINT_OK: return "ok";
+    case GLINT_EINVAL: return "invalid argument";
+    case GLINT_EALIGN: return "pointer not 16-byte aligned or pitch < width";
+    case GLINT_EDEVICE: return "no suitable sm_100 device / context-device mismatch";
+    case GLINT_ELIMIT: return "image too large (>= 2^31 pixels)";
+    case GLINT_ECUDA: return "CUDA runtime error (see glint_last_cuda_error)";
+    case GLINT_ENOMEM: return "allocation failed";
+    default: return "unknown error";
+  }
+}
+
+extern "C" int glint_last_cuda_error(void) { return g_last_cuda; }
+
+// ---------------------------------------------------------------------------
+// Tables. Z[k] = fp32(Phi^-1((k + 1/2)/4096)): Abramowitz & Stegun 26.2.23
+// rational start, then Halley iterations on Phi(x) - q with Phi from erfc,
+// to double precision (the oracle uses a different method: bisection).
+// ---------------------------------------------------------------------------
+static double norm_quantile(double q) {
+  double pp = q < 0.5 ? q : 1.0 - q;
+  double t = sqrt(-2.0 * log(pp));
+  double x = t - (2.515517 + 0.802853 * t + 0.010328 * t * t) /
+                     (1.0 + 1.432788 * t + 0.189269 * t * t + 0.001308 * t * t * t);
+  if (q < 0.5) x = -x;
+  for (int it = 0; it < 6; ++it) {
+    double e = 0.5 * erfc(-x / sqrt(2.0)) - q;
+    double u = e * sqrt(2.0 * M_PI) * exp(0.5 * x * x);
+    double dx = u / (1.0 + 0.5 * x * u);
+    x -= dx;
+    if (fabs(dx) <= 1e-17 * (1.0 + fabs(x))) break;
+  }
+  return x;
+}
+
+extern "C" int glint_build_tables(float* z, float* cosv, float* sinv) {
+  if (z)
+    for (int k = 0; k < GLINT_ZQ; ++k) z[k] = (float)norm_quantile(((double)k + 0.5) / (double)GLINT_ZQ);
+  for (int m = 0; m < GLINT_NANG; ++m) {
+    double ang = (double)m * M_PI / 256.0;
+    if (cosv) cosv[m] = (float)cos(ang);
+    if (sinv) sinv[m] = (float)sin(ang);
+  }
+  return GLINT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Context
+// ---------------------------------------------------------------------------
+extern "C" int glint_create(glint_ctx** out, int device) {
+  if (!out) return GLINT_EINVAL;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+    cudaGetLastError();
+    return GLINT_EDEVICE;
+  }
+  if (device < 0 || device >= ndev) return GLINT_EDEVICE;
+  cudaDeviceProp prop;
+  GL_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0) return GLINT_EDEVICE;   // built for sm_100a only
+  int prev = 0;
+  GL_CUDA(cudaGetDevice(&prev));
+  GL_CUDA(cudaSetDevice(device));
+  glint_ctx* c = new (std::nothrow) glint_ctx();
+  if (!c) return GLINT_ENOMEM;
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  c->launches = 0;
+  int rc = GLINT_OK;
+  float2 cs[GLINT_NANG];
+  glint_build_tables(c->h_z, c->h_cos, c->h_sin);
+  for (int m = 0; m < GLINT_NANG; ++m) cs[m] = make_float2(c->h_cos[m], c->h_sin[m]);
+  cudaError_t e = glint::occupancy_blocks_per_sm(&c->blocks_per_sm);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_z, sizeof(float) * GLINT_ZQ);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cs, sizeof(float2) * GLINT_NANG);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_z, c->h_z, sizeof(float) * GLINT_ZQ, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->d_cs, cs, sizeof(float2) * GLINT_NANG, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    g_last_cuda = (int)e;
+    rc = GLINT_ECUDA;
+    if (c->d_z) cudaFree(c->d_z);
+    if (c->d_cs) cudaFree(c->d_cs);
+    delete c;
+    c = nullptr;
+  } else if (c->blocks_per_sm < 1) {
+    c->blocks_per_sm = 1;
+  }
+  cudaSetDevice(prev);
+  *out = c;
+  return rc;
+}
+
+static void free_stage(glint_ctx* c) {
+  for (int b = 0; b < 2; ++b)
+    for (int p = 0; p < 6; ++p)
+      if (c->d_stage[b][p]) { cudaFree(c->d_stage[b][p]); c->d_stage[b][p] = nullptr; }
+  c->stage_px = 0;
+}
+
+extern "C" int glint_destroy(glint_ctx* c) {
+  if (!c) return GLINT_EINVAL;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(c->device);
+  free_stage(c);
+  for (int b = 0; b < 2; ++b) {
+    if (c->st[b]) cudaStreamDestroy(c->st[b]);
+    if (c->ev_done[b]) cudaEventDestroy(c->ev_done[b]);
+  }
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  cudaFree(c->d_z);
+  cudaFree(c->d_cs);
+  cudaSetDevice(prev);
+  delete c;
+  return GLINT_OK;
+}
+
+extern "C" int glint_get_tables(const glint_ctx* c, float* z, float* cosv, float* sinv) {
+  if (!c) return GLINT_EINVAL;
+  int prev = 0;
+  GL_CUDA(cudaGetDevice(&prev));
+  GL_CUDA(cudaSetDevice(c->device));
+  float2 cs[GLINT_NANG];
+  cudaError_t e = cudaSuccess;
+  if (z) e = cudaMemcpy(z, c->d_z, sizeof(float) * GLINT_ZQ, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(cs, c->d_cs, sizeof(cs), cudaMemcpyDeviceToHost);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) { g_last_cuda = (int)e; return GLINT_ECUDA; }
+  for (int m = 0; m < GLINT_NANG; ++m) {
+    if (cosv) cosv[m] = cs[m].x;
+    if (sinv) sinv[m] = cs[m].y;
+  }
+  return GLINT_OK;
+}
+
+extern "C" int64_t glint_launch_count(const glint_ctx* c) { return c ? c->launches.load() : -1; }
+
+// ---------------------------------------------------------------------------
+// Validation
+// ---------------------------------------------------------------------------
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static int validate_scene(const glint_scene* s) {
+  if (!s) return GLINT_EINVAL;
+  if (s->ndf_kind != 0 && s->ndf_kind != 1) return GLINT_EINVAL;
+  if (s->view_kind != 0 && s->view_kind != 1) return GLINT_EINVAL;
+  if (s->max_ratio_level < 1 || s->max_ratio_level > 8) return GLINT_EINVAL;
+  if (!(s->beta > 0.0f) || !isfinite(s->beta) || s->beta < 0x1p-20f) return GLINT_EINVAL;
+  if (s->n_lights < 0 || s->n_lights > GLINT_MAX_LIGHTS) return GLINT_EINVAL;
+  for (int l = 0; l < s->n_lights; ++l)
+    if (s->lights[l].kind != 0 && s->lights[l].kind != 1) return GLINT_EINVAL;
+  return GLINT_OK;
+}
+
+static int validate_gbuffer(const glint_gbuffer* g, int64_t out_pitch) {
+  if (!g) return GLINT_EINVAL;
+  if (g->width < 0 || g->height < 0) return GLINT_EINVAL;
+  if (g->width == 0 || g->height == 0) return GLINT_OK;
+  if (!g->duv || !g->uvm || !g->nrm || !g->pos || !g->mat) return GLINT_EINVAL;
+  if (g->pitch < g->width || out_pitch < g->width) return GLINT_EALIGN;
+  if (!aligned16(g->duv) || !aligned16(g->uvm) || !aligned16(g->nrm) || !aligned16(g->pos) || !aligned16(g->mat))
+    return GLINT_EALIGN;
+  if ((int64_t)g->width * g->height >= (int64_t)1 << 31) return GLINT_ELIMIT;
+  if (g->pitch * (int64_t)g->height >= (int64_t)1 << 40) return GLINT_ELIMIT;
+  return GLINT_OK;
+}
+
+static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc,
+                                  void* out, int64_t out_pitch, glint_debug_rec* dbg) {
+  glint::KParams k;
+  k.duv = (const float4*)gb->duv;
+  k.uvm = (const float4*)gb->uvm;
+  k.nrm = (const float4*)gb->nrm;
+  k.pos = (const float4*)gb->pos;
+  k.mat = (const float4*)gb->mat;
+  k.out = (float4*)out;
+  k.dbg = dbg;
+  k.ztab = c->d_z;
+  k.cstab = c->d_cs;
+  k.width = gb->width;
+  k.height = gb->height;
+  k.pitch = gb->pitch;
+  k.out_pitch = out_pitch;
+  k.sc = *sc;
+  return k;
+}
+
+static int grid_for(const glint_ctx* c, int64_t n_pix) {
+  int64_t need = (n_pix + glint::kBlock - 1) / glint::kBlock;
+  int64_t cap = (int64_t)c->sm_count * c->blocks_per_sm;
+  return (int)(need < cap ? need : cap);
+}
+
+// ---------------------------------------------------------------------------
+// glint_eval: device buffers, one launch, asynchronous
+// ---------------------------------------------------------------------------
+extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out,
+                          int64_t out_pitch, glint_debug_rec* dbg, void* stream) {
+  if (!c) return GLINT_EINVAL;
+  int rc = validate_scene(sc);
+  if (rc) return rc;
+  rc = validate_gbuffer(gb, out_pitch);
+  if (rc) return rc;
+  if (gb->width == 0 || gb->height == 0) return GLINT_OK;
+  if (!out) return GLINT_EINVAL;
+  if (!aligned16(out)) return GLINT_EALIGN;
+  int cur = -1;
+  GL_CUDA(cudaGetDevice(&cur));
+  if (cur != c->device) return GLINT_EDEVICE;
+  glint::KParams k = make_params(c, gb, sc, out, out_pitch, dbg);
+  int64_t n_pix = (int64_t)gb->width * gb->height;
+  GL_CUDA(glint::launch_eval(k, grid_for(c, n_pix), dbg != nullptr, (cudaStream_t)stream));
+  const_cast<glint_ctx*>(c)->launches++;
+  return GLINT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// glint_eval_host: host planes in, host radiance out; row chunks pipelined
+// over two streams so H2D(chunk c+1) and D2H(chunk c-1) overlap kernel(c).
+// ---------------------------------------------------------------------------
+static int ensure_stage(glint_ctx* c, size_t px) {
+  if (!c->st[0]) {
+    for (int b = 0; b < 2; ++b) {
+      GL_CUDA(cudaStreamCreateWithFlags(&c->st[b], cudaStreamNonBlocking));
+      GL_CUDA(cudaEventCreateWithFlags(&c->ev_done[b], cudaEventDisableTiming));
+    }
+    GL_CUDA(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+  }
+  if (c->stage_px >= px) return GLINT_OK;
+  free_stage(c);
+  for (int b = 0; b < 2; ++b)
+    for (int p = 0; p < 6; ++p) {
+      cudaError_t e = cudaMalloc(&c->d_stage[b][p], px * sizeof(float4));
+      if (e != cudaSuccess) { g_last_cuda = (int)e; free_stage(c); return GLINT_ENOMEM; }
+    }
+  c->stage_px = px;
+  return GLINT_OK;
+}
+
+extern "C" int glint_eval_host(glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out_host,
+                               int64_t out_pitch, void* stream) {
+  if (!c) return GLINT_EINVAL;
+  int rc = validate_scene(sc);
+  if (rc) return rc;
+  rc = validate_gbuffer(gb, out_pitch);
+  if (rc) return rc;
+  if (gb->width == 0 || gb->height == 0) return GLINT_OK;
+  if (!out_host) return GLINT_EINVAL;
+  int cur = -1;
+  GL_CUDA(cudaGetDevice(&cur));
+  if (cur != c->device) return GLINT_EDEVICE;
+  const int W = gb->width, H = gb->height;
+  // ~1M pixels per chunk (80 MB in, 16 MB out), at least 1 row
+  int rows = (int)((1 << 20) / W);
+  if (rows < 1) rows = 1;
+  if (rows > H) rows = H;
+  rc = ensure_stage(c, (size_t)rows * W);
+  if (rc) return rc;
+  GL_CUDA(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
+  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamWaitEvent(c->st[b], c->ev_in, 0));
+  const void* planes[5] = {gb->duv, gb->uvm, gb->nrm, gb->pos, gb->mat};
+  const size_t rowb = (size_t)W * sizeof(float4);
+  int chunk = 0;
+  for (int y0 = 0; y0 < H; y0 += rows, ++chunk) {
+    const int b = chunk & 1;
+    const int nr = (y0 + rows <= H) ? rows : H - y0;
+    cudaStream_t s = c->st[b];
+    for (int p = 0; p < 5; ++p)
+      GL_CUDA(cudaMemcpy2DAsync(c->d_stage[b][p], rowb, (const float4*)planes[p] + (int64_t)y0 * gb->pitch,
+                                (size_t)gb->pitch * sizeof(float4), rowb, nr, cudaMemcpyHostToDevice, s));
+    glint_gbuffer sub;
+    sub.duv = c->d_stage[b][0];
+    sub.uvm = c->d_stage[b][1];
+    sub.nrm = c->d_stage[b][2];
+    sub.pos = c->d_stage[b][3];
+    sub.mat = c->d_stage[b][4];
+    sub.width = W;
+    sub.height = nr;
+    sub.pitch = W;
+    glint::KParams k = make_params(c, &sub, sc, c->d_stage[b][5], W, nullptr);
+    GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
+    c->launches++;
+    GL_CUDA(cudaMemcpy2DAsync((float4*)out_host + (int64_t)y0 * out_pitch, (size_t)out_pitch * sizeof(float4),
+                              c->d_stage[b][5], rowb, rowb, nr, cudaMemcpyDeviceToHost, s));
+  }
+  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamSynchronize(c->st[b]));
+  return GLINT_OK;
+}

@@ -1,0 +1,149 @@
+// glint_device.cuh -- device-side arithmetic of the glint path (sm_100a).
+//
+// Every function here implements one step of the fp32 arithmetic contract of
+// DESIGN.md §4 (bit-exact with the CPU oracle on every value that decides an
+// integer). The translation unit is compiled with -fmad=false so that a*b+c
+// stays two roundings; FMAs appear only as explicit __fmaf_rn where the
+// contract writes fma. No fast-math, no FTZ, IEEE div/sqrt.
+//
+// P:Lnnn = line of the paper's text (arXiv 2306.05051).
+#pragma once
+#include <stdint.h>
+
+namespace glint {
+
+__device__ __forceinline__ float pow2i(int k) { return __uint_as_float((uint32_t)(k + 127) << 23); }
+
+// 2^(e/2) = 2^floor(e/2) * (e odd ? fp32(sqrt 2) : 1)   (grid stretch, Eq. 12 / R-14)
+__device__ __forceinline__ float pow2half(int e) {
+  float s = pow2i(e >> 1);
+  return (e & 1) ? s * 0x1.6a09e6p+0f : s;
+}
+
+// exp2c(y), y <= 0 (Eq. 16 (1-p)^n and the Beckmann exponential). DESIGN §4.2.
+__device__ __forceinline__ float exp2c(float y) {
+  if (!(y >= -125.0f)) return 0.0f;
+  float k = floorf(y + 0.5f);
+  float f = y - k;
+  float q = 0x1.ffcbfcp-17f;
+  q = __fmaf_rn(q, f, 0x1.430912p-13f);
+  q = __fmaf_rn(q, f, 0x1.5d87fep-10f);
+  q = __fmaf_rn(q, f, 0x1.3b2ab6p-7f);
+  q = __fmaf_rn(q, f, 0x1.c6b08ep-5f);
+  q = __fmaf_rn(q, f, 0x1.ebfbe0p-3f);
+  q = __fmaf_rn(q, f, 0x1.62e430p-1f);
+  q = __fmaf_rn(q, f, 1.0f);
+  return q * pow2i((int)k);
+}
+
+// s * atanh(s)/s series to s^15 (Horner in s^2)
+__device__ __forceinline__ float atanh_s(float s) {
+  float z = s * s;
+  float q = 0x1.111112p-4f;
+  q = __fmaf_rn(q, z, 0x1.3b13b2p-4f);
+  q = __fmaf_rn(q, z, 0x1.745d18p-4f);
+  q = __fmaf_rn(q, z, 0x1.c71c72p-4f);
+  q = __fmaf_rn(q, z, 0x1.24924ap-3f);
+  q = __fmaf_rn(q, z, 0x1.99999ap-3f);
+  q = __fmaf_rn(q, z, 0x1.555556p-2f);
+  q = __fmaf_rn(q, z, 1.0f);
+  return s * q;
+}
+
+// log2(1 - p), p in (0, 1). DESIGN §4.2.
+__device__ __forceinline__ float log2_1mp(float p) {
+  if (p < 0.5f) {
+    float s = p / (2.0f - p);
+    return -(atanh_s(s) * 0x1.715476p+1f);
+  }
+  float q = 1.0f - p;
+  uint32_t b = __float_as_uint(q);
+  int e = (int)((b >> 23) & 255u) - 127;
+  float m = __uint_as_float((b & 0x7FFFFFu) | 0x3F800000u);
+  if (m > 0x1.555556p+0f) { m = m * 0.5f; e = e + 1; }
+  float s = (m - 1.0f) / (m + 1.0f);
+  return __fmaf_rn(atanh_s(s), 0x1.715476p+1f, (float)e);
+}
+
+// atan2(y, x) in turns, (-1/2, 1/2]. DESIGN §4.2.
+__device__ __forceinline__ float atan2_turns(float y, float x) {
+  float ax = fabsf(x), ay = fabsf(y);
+  float mx = ax > ay ? ax : ay;
+  float mn = ax > ay ? ay : ax;
+  if (mx == 0.0f) return 0.0f;
+  float t = mn / mx;
+  float base = 0.0f;
+  if (t > 0x1.a8279ap-2f) { t = (t - 1.0f) / (t + 1.0f); base = 0.125f; }
+  float z = t * t;
+  float q = 0x1.32c69ep-7f;
+  q = __fmaf_rn(q, z, -0x1.5bade6p-7f);
+  q = __fmaf_rn(q, z, 0x1.912b1cp-7f);
+  q = __fmaf_rn(q, z, -0x1.da1bacp-7f);
+  q = __fmaf_rn(q, z, 0x1.21bb94p-6f);
+  q = __fmaf_rn(q, z, -0x1.748376p-6f);
+  q = __fmaf_rn(q, z, 0x1.04c26cp-5f);
+  q = __fmaf_rn(q, z, -0x1.b2995ep-5f);
+  q = __fmaf_rn(q, z, 0x1.45f306p-3f);
+  float a = __fmaf_rn(t, q, base);
+  if (ay > ax) a = 0.25f - a;
+  if (x < 0.0f) a = 0.5f - a;
+  if (y < 0.0f) a = -a;
+  return a;
+}
+
+// published "lowbias32" mixer (R-23)
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+// second half of lowbias32 given x already xor-shifted by 16 (draw hash, S7)
+__device__ __forceinline__ uint32_t lowbias32_tail(uint32_t x) {
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ float dot3(float ax, float ay, float az, float bx, float by, float bz) {
+  return __fmaf_rn(az, bz, __fmaf_rn(ay, by, ax * bx));
+}
+__device__ __forceinline__ void normalize3(float& x, float& y, float& z) {
+  float l2 = dot3(x, y, z, x, y, z);
+  float inv = 1.0f / sqrtf(l2);
+  x = x * inv; y = y * inv; z = z * inv;
+}
+
+// Gate parameters of one grid (Eq. 16-17, readings R-1..R-4). DESIGN §4.3 S6.
+struct Gate {
+  uint32_t T;
+  float sigma, m1, cap;
+};
+__device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
+  // L2 = log2(1 - p) for p in (0,1), precomputed once per (pixel, light)
+  Gate g;
+  if (!(n > 0.0f) || !(p > 0.0f)) { g.T = 0; g.sigma = 0.0f; g.m1 = 1.0f; g.cap = 1.0f; return g; }
+  float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
+  g.T = (uint32_t)ceilf(pge1 * 0x1p23f);
+  float nm1 = n - 1.0f;
+  float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
+  g.sigma = sqrtf(mu * (1.0f - p));
+  g.m1 = 1.0f + mu;
+  g.cap = ceilf(n);
+  return g;
+}
+
+// One gated draw (Eq. 18): h -> theta0 gate (bits 9..31) and z = Z[h & 4095].
+__device__ __forceinline__ float gated_count(uint32_t h, const Gate& g, const float* sZ) {
+  float z = sZ[h & 4095u];
+  float x = __fmaf_rn(g.sigma, z, g.m1);
+  x = x < 1.0f ? 1.0f : x;
+  x = x > g.cap ? g.cap : x;
+  return ((h >> 9) < g.T) ? floorf(x) : 0.0f;
+}
+
+}  // namespace glint

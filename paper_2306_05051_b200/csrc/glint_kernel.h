@@ -1,0 +1,30 @@
+// glint_kernel.h -- internal launch interface between the host API and the kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/glint.h"
+
+namespace glint {
+
+constexpr int kBlock = 256;
+
+struct KParams {
+  const float4* duv;
+  const float4* uvm;
+  const float4* nrm;
+  const float4* pos;
+  const float4* mat;
+  float4* out;
+  glint_debug_rec* dbg;
+  const float* ztab;    // GLINT_ZQ floats (device)
+  const float2* cstab;  // GLINT_NANG (cos, sin) pairs (device)
+  int32_t width, height;
+  int64_t pitch, out_pitch;
+  glint_scene sc;
+};
+
+cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream);
+cudaError_t occupancy_blocks_per_sm(int* out);
+
+}  // namespace glint

@@ -75,7 +75,7 @@ def test_hashed_draws_follow_the_enumerated_law(orc):
     h = r["hash"][:, :12].ravel()
     c = r["count"][:, :12].ravel()
     _, first = np.unique(h, return_index=True)          # each (texel, node) once
-    c = c[first]
+    c = c[first].astype(np.int64)
     assert len(c) > 10000
     pmf, (T, *_rest) = stats.gated_pmf_enumerated(float(r["n"][0, 0]), float(r["p"][0]))
     assert T == r["T"][0, 0]
