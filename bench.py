@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the glint hot path (BASELINE.json metric: glint shading
+evals/s, one eval = one valid pixel x one light = 48 gated binomial draws).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C4]
+
+One step = one pass of the whole hot path (S0-S9) over one
+batch of synthetic input: for C2 (default, BASELINE.json configs[1]) the
+10-elevation set of 1920x1080 ground-plane frames, one point light. Inputs
+are resident in HBM when the timed region starts; they total 1.66 GB per
+rank (> 126 MB L2), so no L2 flush is needed between steps. For N > 1
+(torchrun) every rank shades its own frame set (hash seed differs per rank),
+no data-path collective: weak scaling, value = evals of all ranks / max-over-
+ranks device time.
+
+Prints ONE JSON line on rank 0. ``--impl reference`` times the CPU oracle
+(oracle/) on the host cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "glint shading evals/s (pixel x light) at 1/2/4/8 B200; % of FP32 peak"
+UNIT = "evals/s"
+# Algorithmic work per eval (SURVEY §8d budget): 340 thread
+# instructions per pixel (S0-S4a, shared by the L lights) + 1110 per
+# (pixel, light) (S5-S9, of which 860 are the 48 draws).
+W_PIXEL, W_EVAL = 340.0, 1110.0
+# Algorithmic HBM bytes per pixel: 5 float4 planes in + 1 float4 out.
+BYTES_PER_PIXEL = 96.0
+SM_COUNT_B200 = 148
+LANES_PER_SM = 128
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4, "hw_slowdown": 0x8,
+        "sync_boost": 0x10, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+        "hw_power_brake_slowdown": 0x80, "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"], "samples": 0}
+        names = [k for k, v in self.REASONS.items() if self.reasons & v and k != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+    def rejected(self):
+        bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+        s = self.summary()
+        if set(s["reasons"]) & bad:
+            return True
+        if s["sm_mhz"] and s["sm_max_mhz"] and s["sm_mhz"] < 0.6 * s["sm_max_mhz"] and not s["reasons"]:
+            return True
+        return False
+
+
+# ----------------------------------------------------------------------------- workload
+def make_frames(config: str, device, seed: int):
+    from paper_2306_05051_b200 import synth
+    if config == "C2":
+        frames = synth.c2_frames(device=device)
+        desc = ("C2: 1920x1080 infinite ground plane, pinhole 60deg FOV, elevations 5..85 + 90 deg "
+                "(10 frames per step), 1 point light, GGX alpha 0.2, N = 2^U(8,20) per uv tile, R = 0.034")
+    elif config == "C4":
+        frames = [synth.c4(f, device=device) for f in range(8)]
+        desc = ("C4: 3840x2160, 32 spheres on a plane, anisotropic GGX alpha U(0.05,0.6), N log-U[1e3,1e7], "
+                "16 point lights, 8 jittered frames per step")
+    else:
+        raise SystemExit(f"unknown config {config}")
+    for fr in frames:
+        fr.scene.seed = seed
+    return frames, desc
+
+
+def count_evals(frames):
+    tot_px = sum(fr.gbuf.height * fr.gbuf.width for fr in frames)
+    evals = sum(fr.gbuf.valid_count() * len(fr.scene.lights) for fr in frames)
+    valid_px = sum(fr.gbuf.valid_count() for fr in frames)
+    return tot_px, valid_px, evals
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_sample(frames, row_stride: int):
+    """Deterministic bounded sample of the workload: every ``row_stride``-th row
+    of every frame (all lights), as host arrays."""
+    from paper_2306_05051_b200 import synth
+    subs = []
+    for fr in frames:
+        gb = synth.GBuffer(*[p[::row_stride].contiguous().cpu() for p in fr.gbuf.planes()])
+        subs.append((gb, fr.scene))
+    return subs
+
+
+def time_oracle(subs, threads=None):
+    import oracle
+    t0 = time.perf_counter()
+    ev = 0
+    for gb, sc in subs:
+        oracle.eval(gb, sc, threads=threads)
+        ev += gb.valid_count() * len(sc.lights)
+    return ev, time.perf_counter() - t0
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def run_reference(args):
+    from paper_2306_05051_b200 import dist as D
+    rank, world, _ = D.env_rank_world()
+    if rank != 0:
+        return 0
+    frames, desc = make_frames(args.config, "cpu", seed=1)
+    stride = 64 if args.config == "C2" else 256
+    subs = oracle_sample(frames, stride)
+    cores = host_cores()
+    for _ in range(args.warmup):
+        time_oracle(subs)
+    ev_tot, t_tot = 0, 0.0
+    for _ in range(args.steps):
+        ev, t = time_oracle(subs)
+        ev_tot += ev
+        t_tot += t
+    value = ev_tot / t_tot
+    sample = f"every {stride}th row of each of the {len(frames)} frames of {args.config} ({ev_tot // args.steps} evals/step)"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "config": {"workload": desc, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def read_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get("dram_bytes_per_launch_per_pixel"), d
+
+
+def run_ours(args):
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import build as B
+    from paper_2306_05051_b200 import dist as D
+    if int(os.environ.get("RANK", "0")) == 0:
+        B.build()
+    rank, world, local = D.init("nccl")
+    if world > 1:
+        D.barrier()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ctx = pkg.Context(local)
+    frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank)
+    tot_px, valid_px, evals = count_evals(frames)
+    outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
+    stream = torch.cuda.current_stream(dev)
+
+    def step(evs=None):
+        for i, (fr, out) in enumerate(zip(frames, outs)):
+            if evs is not None:
+                evs[i][0].record(stream)
+            pkg.glint_eval(ctx, fr.gbuf, fr.scene, out=out, stream=stream)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    args.warmup = max(args.warmup, 3)      # contract: W >= 3
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    def timed():
+        ev_pairs = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+                     for _ in frames] for _ in range(args.steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0 = ctx.launch_count()
+        with ClockSampler(local) as clk:
+            D.barrier()
+            torch.cuda.synchronize()
+            start.record(stream)
+            for k in range(args.steps):
+                step(ev_pairs[k])
+            end.record(stream)
+            torch.cuda.synchronize()
+            D.barrier()
+        ms = start.elapsed_time(end)
+        launch_ms = [a.elapsed_time(b) for st in ev_pairs for a, b in st]
+        return ms, launch_ms, ctx.launch_count() - n0, clk
+
+    ms, launch_ms, launches, clk = timed()
+    if clk.rejected():
+        ms, launch_ms, launches, clk = timed()
+    ms_max = D.max_over_ranks(ms, device=dev)
+    evals_all = D.sum_over_ranks(evals * args.steps, device=dev)
+    value = evals_all / (ms_max / 1e3)
+
+    # ---- roofline of the dominant (only) kernel: issue-bound ALU path
+    peaks, peak_src = load_peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    issue_peak = sms * LANES_PER_SM * f_max                   # thread-instructions/s
+    L = len(frames[0].scene.lights)
+    w_eval = W_EVAL + W_PIXEL / L
+    mean_launch_s = float(np.mean(launch_ms)) / 1e3
+    evals_per_launch = evals / len(frames)
+    achieved = evals_per_launch * w_eval / mean_launch_s
+    traffic_pp, prof = read_profile_traffic()
+    px_per_launch = tot_px / len(frames)
+    roofline = {
+        "bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "thread-inst/s",
+        "frac": achieved / issue_peak,
+        "traffic": (traffic_pp * px_per_launch) if traffic_pp else None,
+        "peak_source": f"{sms} SMs x 128 lanes x sm_max_mhz {f_max / 1e6:.0f} ({peak_src} MEASURED_PEAKS.json)",
+        "algorithmic_inst_per_eval": w_eval,
+        "hbm_achieved_gbs": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9,
+        "hbm_frac": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9 / float(peaks.get("hbm_gbs", 6458.7)),
+        "mean_launch_ms": mean_launch_s * 1e3,
+    }
+    if prof and prof.get("sass_thread_inst_per_eval"):
+        roofline["sass_thread_inst_per_eval"] = prof["sass_thread_inst_per_eval"]
+        roofline["issue_frac_sass"] = evals_per_launch * prof["sass_thread_inst_per_eval"] / mean_launch_s / issue_peak
+    cs = clk.summary()
+    if cs.get("sm_mhz"):
+        roofline["frac_at_measured_clock"] = achieved / (sms * LANES_PER_SM * cs["sm_mhz"] * 1e6)
+
+    # ---- end to end through the public C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        hosts = [fr.gbuf.to("cpu").pin() for fr in frames]
+        houts = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32).pin_memory() for fr in frames]
+        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        for hb, fr, ho in zip(hosts, frames, houts):
+            pkg.glint_eval_host(ctx, hb, fr.scene, out=ho)
+        D.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            for hb, fr, ho in zip(hosts, frames, houts):
+                pkg.glint_eval_host(ctx, hb, fr.scene, out=ho)
+        torch.cuda.synchronize()
+        t_e2e = D.max_over_ranks(time.perf_counter() - t0, device=dev)
+        e2e = {"value": D.sum_over_ranks(evals * n_e2e, device=dev) / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(tot_px * 80), "d2h_bytes_per_step": int(tot_px * 16),
+               "steps": n_e2e, "api": "glint_eval_host (pinned host G-buffer -> host radiance)"}
+        # sanity: host path reproduces the device path bit for bit
+        if not torch.equal(houts[0].view(torch.int32), outs[0].cpu().view(torch.int32)):
+            raise SystemExit("glint_eval_host output differs from glint_eval")
+
+    # ---- CPU baseline (oracle on host cores), rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        stride = 32 if args.config == "C2" else 256
+        subs = oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride)
+        ev, t = time_oracle(subs)
+        cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
+               "sample": f"every {stride}th row of each of the {len(frames)} frames ({ev} evals, {t:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "pixels_per_step": tot_px, "valid_pixels_per_step": valid_px,
+                       "evals_per_step_per_rank": evals, "lights": L, "launches_per_step": len(frames),
+                       "l2": "inputs 1.66 GB per rank > 126 MB L2: no flush between steps",
+                       "parallelism": f"frames x{world} ranks, no data-path collective"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": cs, "gpu": props.name,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

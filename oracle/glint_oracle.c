@@ -159,6 +159,16 @@ uint32_t orc_lowbias32(uint32_t x) {
   return x;
 }
 
+/* the last four steps of lowbias32; the per-draw hash is tail(hs + ka) of
+ * the spatial seed hs and the angular seed ka (both full lowbias32 outputs) */
+uint32_t orc_lowbias32_tail(uint32_t x) {
+  x *= 0x7feb352dU;
+  x ^= x >> 15;
+  x *= 0x846ca68bU;
+  x ^= x >> 16;
+  return x;
+}
+
 /* ---------------------------------------------------------------------- */
 /* S1  Footprint: "we use screen-space derivatives to obtain the
  * minor/major axis"; phi = orientation of the major axis v0, r = |v0|/|v1|.
@@ -333,7 +343,8 @@ void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]) 
 /* S6  Gated Gaussian binomial (Eq. 16-18, readings R-1..R-4):
  * P>=1 = 1 - (1-p)^n; mu = (n-1)p, sigma = sqrt((n-1)p(1-p)); gate succeeds
  * iff theta0 < P>=1 with theta0 = (h >> 9) 2^-23, i.e. (h >> 9) < T where
- * T = ceil(P>=1 2^23); count = clamp(floor(1 + mu + sigma z), 1, ceil(n)).   */
+ * T = ceil(P>=1 2^23); z = Z[(h >> 2) & 4095] (bits 2..13);
+ * count = floor(clamp(1 + mu + sigma z, 1, ceil(n))) (reading R-3).         */
 /* ---------------------------------------------------------------------- */
 void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap) {
   if (!(n > 0.0f) || !(p > 0.0f)) { *T = 0; *sigma = 0.0f; *m1 = 1.0f; *cap = 1.0f; return; }
@@ -355,7 +366,7 @@ void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, flo
 float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap) {
   orc_init();
   if (!((h >> 9) < T)) return 0.0f;               /* H(P>=1 - theta0) gate, R-1 */
-  float z = g_z[h & (ORC_ZQ - 1)];                /* N(theta1) via quantile table, R-2 */
+  float z = g_z[(h >> 2) & (ORC_ZQ - 1)];         /* N(theta1) via quantile table, R-2 */
   float x = fmaf(sigma, z, m1);                   /* 1 + N(theta1; mu, sigma) */
   x = x < 1.0f ? 1.0f : x;                        /* R-3 clamp */
   x = x > cap ? cap : x;
@@ -385,7 +396,7 @@ static float exact_count(uint32_t h, float n, float p) {
 /* ---------------------------------------------------------------------- */
 float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz) {
   if (!(hz > 0.0f)) return 0.0f;
-  float X = hx / ax, Y = hy / ay;
+  float X = hx * (1.0f / ax), Y = hy * (1.0f / ay);
   float s2 = X * X + Y * Y;
   float hz2 = hz * hz;
   if (ndf_kind == 0) {
@@ -497,11 +508,12 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       if (fx >= fy) { betad[i][0] = 1.0 - fx; betad[i][1] = fx - fy; betad[i][2] = fy; }
       else          { betad[i][0] = 1.0 - fy; betad[i][1] = fy - fx; betad[i][2] = fx; }
     }
+    /* spatial seed of texel (grid key, lattice vertex): one hash of the
+     * object/seed word plus a linear code of (key, lx, ly) (reading R-23) */
     uint32_t gk = ((uint32_t)ls[i] & 511u) | ((uint32_t)lr[i] << 9) | ((uint32_t)jo[i] << 13);
-    uint32_t g = orc_lowbias32(so ^ gk);
     for (int k = 0; k < 3; ++k) {
-      uint32_t lin = (uint32_t)lxs[i][k] * 0x8da6b343U + (uint32_t)lys[i][k] * 0xd8163841U;
-      hs[i][k] = orc_lowbias32(g ^ lin);
+      uint32_t lin = gk * 0x9e3779b1U + (uint32_t)lxs[i][k] * 0x8da6b343U + (uint32_t)lys[i][k] * 0xd8163841U;
+      hs[i][k] = orc_lowbias32(so + lin);
     }
   }
 
@@ -535,15 +547,18 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       for (int i = 0; i < 4; ++i) { rc->ls[i] = ls[i]; rc->lr[i] = lr[i]; rc->jo[i] = jo[i]; rc->w[i] = w[i]; rc->n[i] = n[i]; }
       for (int i = 0; i < 4; ++i) for (int k = 0; k < 3; ++k) { rc->lx[i*3+k] = (int32_t)(uint32_t)lxs[i][k]; rc->ly[i*3+k] = (int32_t)(uint32_t)lys[i][k]; }
     }
-    /* S5: light direction (P:L1228 punctual lights only, reading R-27) */
-    float wo[3];
-    if (lt->kind == 0) { wo[0] = lt->pos_or_dir[0] - pos[0]; wo[1] = lt->pos_or_dir[1] - pos[1]; wo[2] = lt->pos_or_dir[2] - pos[2]; }
-    else { wo[0] = lt->pos_or_dir[0]; wo[1] = lt->pos_or_dir[1]; wo[2] = lt->pos_or_dir[2]; }
-    normalize3f(wo);
-    float no = dot3f(nf, wo);
-    if (!(ni > 0.0f && no > 0.0f)) continue; /* light below the horizon: 0 */
+    /* S5: light direction d toward the light (P:L1228 punctual lights only,
+     * reading R-27); w_o = d/|d|. The light is active iff n.w_i > 0 and
+     * n.d > 0; h = normalize(|d| w_i + d), proportional to w_i + w_o. */
+    float d[3];
+    if (lt->kind == 0) { d[0] = lt->pos_or_dir[0] - pos[0]; d[1] = lt->pos_or_dir[1] - pos[1]; d[2] = lt->pos_or_dir[2] - pos[2]; }
+    else { d[0] = lt->pos_or_dir[0]; d[1] = lt->pos_or_dir[1]; d[2] = lt->pos_or_dir[2]; }
+    float d2 = dot3f(d, d);
+    float n_d = dot3f(nf, d);
+    if (!(ni > 0.0f && n_d > 0.0f)) continue; /* light below the horizon: 0 */
     if (rc) rc->light_active = 1;
-    float hv[3] = {wi[0] + wo[0], wi[1] + wo[1], wi[2] + wo[2]};
+    float dl = sqrtf(d2);
+    float hv[3] = {fmaf(dl, wi[0], d[0]), fmaf(dl, wi[1], d[1]), fmaf(dl, wi[2], d[2])};
     normalize3f(hv);
     float hx = dot3f(hv, tf), hy = dot3f(hv, bf), hz = dot3f(hv, nf);
     /* Eq. 4: p = R D(h)/D(n), clamped to 1 (reading R-19) */
@@ -573,7 +588,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       for (int k = 0; k < 3; ++k) {
         double Cik = 0.0;
         for (int jn = 0; jn < 4; ++jn) {
-          uint32_t h = orc_lowbias32(hs[i][k] ^ ka[jn]);
+          uint32_t h = orc_lowbias32_tail(hs[i][k] + ka[jn]);
           float c = sc->sampler == 1 ? exact_count(h, n[i], p) : orc_gated_count(h, T, sig, m1, cap);
           if (rc) { rc->hash[i*12 + k*4 + jn] = h; rc->count[i*12 + k*4 + jn] = c; }
           Cik += vj[jn] * (double)c;

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libglint.so")
 SOURCES = ["glint_kernel.cu", "glint_api.cu"]
-HEADERS = ["glint_kernel.h", "glint_device.cuh", os.path.join("..", "..", "include", "glint.h")]
+HEADERS = ["glint_kernel.h", "glint_device.cuh", "glint_tma.cuh", os.path.join("..", "..", "include", "glint.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -100,15 +100,6 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
   x ^= x >> 16;
   return x;
 }
-// second half of lowbias32 given x already xor-shifted by 16 (draw hash, S7)
-__device__ __forceinline__ uint32_t lowbias32_tail(uint32_t x) {
-  x *= 0x7feb352dU;
-  x ^= x >> 15;
-  x *= 0x846ca68bU;
-  x ^= x >> 16;
-  return x;
-}
-
 __device__ __forceinline__ float dot3(float ax, float ay, float az, float bx, float by, float bz) {
   return __fmaf_rn(az, bz, __fmaf_rn(ay, by, ax * bx));
 }
@@ -135,15 +126,6 @@ __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   g.m1 = 1.0f + mu;
   g.cap = ceilf(n);
   return g;
-}
-
-// One gated draw (Eq. 18): h -> theta0 gate (bits 9..31) and z = Z[h & 4095].
-__device__ __forceinline__ float gated_count(uint32_t h, const Gate& g, const float* sZ) {
-  float z = sZ[h & 4095u];
-  float x = __fmaf_rn(g.sigma, z, g.m1);
-  x = x < 1.0f ? 1.0f : x;
-  x = x > g.cap ? g.cap : x;
-  return ((h >> 9) < g.T) ? floorf(x) : 0.0f;
 }
 
 }  // namespace glint

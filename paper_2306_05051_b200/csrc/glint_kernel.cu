@@ -7,15 +7,19 @@
 // grids, S7 the 48 gated draws (fully unrolled, hashes finished in
 // registers, quantiles from a shared-memory table), S8 blend, S9 radiance.
 //
-// The block count is capped at (#SMs x resident blocks per SM) and blocks
-// stride over the image, so the 18 KB of tables are staged into shared memory
-// once per resident block, not once per 256 pixels.
+// Persistent grid: the block count is capped at (#SMs x resident blocks per
+// SM) and blocks stride over 256-pixel tiles, so the 18 KB of tables are staged
+// into shared memory once per resident block. For contiguous G-buffers the
+// next tile's 5 planes (20 KB) are streamed HBM -> shared memory by the TMA
+// bulk-copy engine (cp.async.bulk + mbarrier, double-buffered) while the
+// current tile is shaded, so the DRAM latency is off the critical path.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/glint.h"
 #include "glint_device.cuh"
 #include "glint_kernel.h"
+#include "glint_tma.cuh"
 
 namespace glint {
 
@@ -59,59 +63,50 @@ __device__ __forceinline__ void lattice(float P, float r, float psi, int K, Slot
   int kA11 = ((er + 1) << 9) | (2 * j + 1);
   int kA12 = ((er + 1) << 9) | ((2 * j + 2) & (nO - 1));
 
-  int k0, k1, k2;
-  float w0, w1, w2;
-  float ht = 0.5f * tr;
-  if (a <= ht) {                       // T0 = {A00, A10, A11}
-    k0 = kA00; k1 = kA10; k2 = kA11;
-    w0 = 1.0f - tr;
-    w2 = a + a;
-    w1 = tr - w2;
-  } else if (a >= 1.0f - ht) {         // T2 = {A01, A11, A12}
-    float om = 1.0f - a;
-    k0 = kA01; k1 = kA11; k2 = kA12;
-    w0 = 1.0f - tr;
-    w1 = om + om;
-    w2 = tr - w1;
-  } else {                             // T1 = {A00, A11, A01}
-    k0 = kA00; k1 = kA11; k2 = kA01;
-    w0 = (1.0f - a) - ht;
-    w1 = tr;
-    w2 = a - ht;
-  }
+  // triangle of the pentagon (tr, a) (R-11), branch-free: every candidate
+  // weight is computed with the contract's ops and selected (same bits)
+  const float ht = 0.5f * tr;
+  const bool c0 = a <= ht;                    // T0 = {A00, A10, A11}
+  const bool c2 = !c0 && (a >= 1.0f - ht);    // T2 = {A01, A11, A12}; else T1 = {A00, A11, A01}
+  const float om = 1.0f - a;
+  const float two_a = a + a, two_om = om + om;
+  const float omt = 1.0f - tr;
+  int k0 = c2 ? kA01 : kA00;
+  int k1 = c0 ? kA10 : kA11;
+  int k2 = c0 ? kA11 : (c2 ? kA12 : kA01);
+  float w0 = (c0 || c2) ? omt : (om - ht);
+  float w1 = c0 ? (tr - two_a) : (c2 ? two_om : tr);
+  float w2 = c0 ? two_a : (c2 ? (tr - two_om) : (a - ht));
   // merge coincident vertices (ring 0), in (0,1), (0,2), (1,2) order (R-13)
-  if (k1 == k0) { w0 = w0 + w1; w1 = 0.0f; }
-  if (k2 == k0) { w0 = w0 + w2; w2 = 0.0f; }
-  if (k2 == k1) { w1 = w1 + w2; w2 = 0.0f; }
+  { const bool m = k1 == k0; w0 = m ? w0 + w1 : w0; w1 = m ? 0.0f : w1; }
+  { const bool m = k2 == k0; w0 = m ? w0 + w2 : w0; w2 = m ? 0.0f : w2; }
+  { const bool m = k2 == k1; w1 = m ? w1 + w2 : w1; w2 = m ? 0.0f : w2; }
   // stable sort by key: compare-swaps (0,1), (1,2), (0,1)  (R-12 global order)
-#define GL_CSWAP(ka, wa, kb, wb) \
-  if (ka > kb) { int tk = ka; ka = kb; kb = tk; float tw = wa; wa = wb; wb = tw; }
+#define GL_CSWAP(ka, wa, kb, wb)                                 \
+  {                                                              \
+    const bool sw = ka > kb;                                     \
+    const int tk = sw ? kb : ka; kb = sw ? ka : kb; ka = tk;      \
+    const float tw = sw ? wb : wa; wb = sw ? wa : wb; wa = tw;    \
+  }
   GL_CSWAP(k0, w0, k1, w1);
   GL_CSWAP(k1, w1, k2, w2);
   GL_CSWAP(k0, w0, k1, w1);
 #undef GL_CSWAP
   // prism -> 3 tetrahedra, staircase fill of the top level (R-12)
-  float al = w0, be = w1, ga = w2;
-  float t = ts;
-  float ab = al + be;
+  const float al = w0, be = w1, ga = w2;
+  const float t = ts;
+  const float ab = al + be;
+  const bool s0 = t <= al, s1 = !s0 && (t <= ab);   // else s2
   int kk[4], ll[4];
   float ww[4];
-  if (t <= al) {
-    kk[0] = k0; ll[0] = es;     ww[0] = al - t;
-    kk[1] = k1; ll[1] = es;     ww[1] = be;
-    kk[2] = k2; ll[2] = es;     ww[2] = ga;
-    kk[3] = k0; ll[3] = es + 1; ww[3] = t;
-  } else if (t <= ab) {
-    kk[0] = k1; ll[0] = es;     ww[0] = ab - t;
-    kk[1] = k2; ll[1] = es;     ww[1] = ga;
-    kk[2] = k0; ll[2] = es + 1; ww[2] = al;
-    kk[3] = k1; ll[3] = es + 1; ww[3] = t - al;
-  } else {
-    kk[0] = k2; ll[0] = es;     ww[0] = 1.0f - t;
-    kk[1] = k0; ll[1] = es + 1; ww[1] = al;
-    kk[2] = k1; ll[2] = es + 1; ww[2] = be;
-    kk[3] = k2; ll[3] = es + 1; ww[3] = (t - al) - be;
-  }
+  kk[0] = s0 ? k0 : (s1 ? k1 : k2); ll[0] = es;
+  ww[0] = s0 ? al - t : (s1 ? ab - t : 1.0f - t);
+  kk[1] = s0 ? k1 : (s1 ? k2 : k0); ll[1] = (s0 || s1) ? es : es + 1;
+  ww[1] = s0 ? be : (s1 ? ga : al);
+  kk[2] = s0 ? k2 : (s1 ? k0 : k1); ll[2] = s0 ? es : es + 1;
+  ww[2] = s0 ? ga : (s1 ? al : be);
+  kk[3] = s0 ? k0 : (s1 ? k1 : k2); ll[3] = es + 1;
+  ww[3] = s0 ? t : (s1 ? t - al : (t - al) - be);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     s[i].ls = ll[i];
@@ -122,262 +117,353 @@ __device__ __forceinline__ void lattice(float P, float r, float psi, int K, Slot
 }
 
 // fp32 Smith Lambda for the radiance path (R-21)
+// (tolerance path: MUFU-based approximations, |rel err| ~1e-7)
 __device__ __forceinline__ float smith_lambda(int kind, float ax2, float ay2, float wx, float wy, float wz) {
-  float s = ax2 * (wx * wx) + ay2 * (wy * wy);
+  const float s = __fmaf_rn(ax2, wx * wx, ay2 * (wy * wy));
   if (!(s > 0.0f)) return 0.0f;
   if (kind == 0) {
-    float q = s / (wz * wz);
-    return q / (2.0f * (1.0f + sqrtf(1.0f + q)));
+    const float q = __fdividef(s, wz * wz);
+    const float r1 = 1.0f + q;
+    return __fdividef(q, 2.0f * (1.0f + r1 * rsqrtf(r1)));
   }
-  float a = wz * rsqrtf(s);
+  const float a = wz * rsqrtf(s);
   if (a >= 1.6f) return 0.0f;
-  return __fdividef(1.0f - 1.259f * a + 0.396f * a * a, 3.535f * a + 2.181f * a * a);
+  return __fdividef(__fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f), a * __fmaf_rn(2.181f, a, 3.535f));
 }
 
 // ---------------------------------------------------------------------------
-// The kernel
+// Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
+// pixel's output float4, `rec` its first debug record (DEBUG only).
 // ---------------------------------------------------------------------------
 template <bool DEBUG>
-__global__ void __launch_bounds__(kBlock) glint_eval_kernel(const KParams prm) {
-  __shared__ float sZ[GLINT_ZQ];
-  __shared__ float2 sCS[GLINT_NANG];
-  for (int i = threadIdx.x; i < GLINT_ZQ; i += kBlock) sZ[i] = prm.ztab[i];
-  for (int i = threadIdx.x; i < GLINT_NANG; i += kBlock) sCS[i] = prm.cstab[i];
+__device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
+                                            const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
+                                            float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
+                                            uint32_t seed_h, float inv_beta) {
+  const int L = sc.n_lights;
+  uint32_t flags = 0;
+  const uint32_t meta = __float_as_uint(uvm.w);
+  const float u = uvm.x, v = uvm.y;
+  bool ok = (meta & 1u) != 0;
+  if (!ok) flags = GLINT_FLAG_INVALID;
+  if (ok && !(fabsf(u) <= 0x1p24f && fabsf(v) <= 0x1p24f)) {
+    flags = GLINT_FLAG_INVALID | GLINT_FLAG_UV_RANGE;
+    ok = false;
+  }
+  // ---------------- S1: footprint (R-7, R-8)
+  float P = 0.0f, r = 0.0f, psi = 0.0f;
+  if (ok) {
+    const float dudx = duv.x, dvdx = duv.y, dudy = duv.z, dvdy = duv.w;
+    const float det = dudx * dvdy - dvdx * dudy;
+    const float a = dudx * dudx + dudy * dudy;
+    const float b = dudx * dvdx + dudy * dvdy;
+    const float c = dvdx * dvdx + dvdy * dvdy;
+    const float hm = 0.5f * (a - c);
+    const float disc = sqrtf(hm * hm + b * b);
+    const float lam = 0.5f * (a + c) + disc;
+    P = fabsf(det);
+    r = lam / P;
+    const float at = atan2_turns(2.0f * b, a - c);
+    psi = at < 0.0f ? at + 1.0f : at;
+    if (psi >= 1.0f) psi = 0.0f;
+    if (!(P >= 0x1p-64f && P < 0x1p64f)) {
+      flags = GLINT_FLAG_DEGENERATE;
+      ok = false;
+    }
+  }
+  if (!ok) {
+    __stcs(outp, make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(flags)));
+    if (DEBUG) {
+      for (int l = 0; l < L; ++l) {
+        uint32_t* w = reinterpret_cast<uint32_t*>(rec + l);
+        for (int q = 0; q < (int)(sizeof(glint_debug_rec) / 4); ++q) w[q] = 0u;
+        rec[l].flags = flags;
+      }
+    }
+    return;
+  }
+
+  // ---------------- S2: 4 grids + distribution weights, n_i = w_i N 2^ls
+  Slot sl[4];
+  lattice(P, r, psi, sc.max_ratio_level, sl, flags);
+  const float ax = mat.x, ay = mat.y, N = mat.z, R = mat.w;
+  float n[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) n[i] = sl[i].w * (N * pow2i(sl[i].ls));
+
+  // ---------------- S3 + S4a: grid transform, simplex, spatial seeds (12)
+  // hsC = hs * C1: the draw hash tail(hs + ka) starts with (hs + ka) * C1 =
+  // hsC + kaC, one add per draw.
+  const uint32_t so = lowbias32(__float_as_uint(uvm.z) ^ seed_h);
+  uint32_t hsC[12];
+  float beta[12];
+  uint32_t dlx[DEBUG ? 12 : 1], dly[DEBUG ? 12 : 1], dhs[DEBUG ? 12 : 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 cs = sCS[sl[i].jo << (8 - sl[i].lr)];
+    const float xr = __fmaf_rn(cs.x, u, cs.y * v);
+    const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
+    const float gx = xr * pow2half(-(sl[i].ls + sl[i].lr));
+    const float gy = yr * pow2half(sl[i].lr - sl[i].ls);
+    const float xs = gx + 0.5f * gy;
+    const float fxs = floorf(xs), fys = floorf(gy);
+    const float fx = xs - fxs, fy = gy - fys;
+    const uint32_t ix = (uint32_t)(long long)fxs, iy = (uint32_t)(long long)fys;
+    const bool lower = fx >= fy;
+    beta[i * 3 + 0] = 1.0f - (lower ? fx : fy);
+    beta[i * 3 + 1] = lower ? fx - fy : fy - fx;
+    beta[i * 3 + 2] = lower ? fy : fx;
+    const uint32_t key = ((uint32_t)sl[i].ls & 511u) | ((uint32_t)sl[i].lr << 9) | ((uint32_t)sl[i].jo << 13);
+    // seed of texel (key; lattice vertex): lowbias32(so + key K + lx A + ly B);
+    // vertices (ix,iy), lower ? (ix+1,iy) : (ix,iy+1), (ix+1,iy+1)
+    const uint32_t base = so + key * 0x9e3779b1U + ix * 0x8da6b343U + iy * 0xd8163841U;
+    const uint32_t lin1 = base + (lower ? 0x8da6b343U : 0xd8163841U);
+    const uint32_t lin2 = base + (0x8da6b343U + 0xd8163841U);
+    const uint32_t h0 = lowbias32(base), h1 = lowbias32(lin1), h2 = lowbias32(lin2);
+    hsC[i * 3 + 0] = h0 * 0x7feb352dU;
+    hsC[i * 3 + 1] = h1 * 0x7feb352dU;
+    hsC[i * 3 + 2] = h2 * 0x7feb352dU;
+    if (DEBUG) {
+      dlx[i * 3 + 0] = ix; dly[i * 3 + 0] = iy;
+      dlx[i * 3 + 1] = lower ? ix + 1u : ix; dly[i * 3 + 1] = lower ? iy : iy + 1u;
+      dlx[i * 3 + 2] = ix + 1u; dly[i * 3 + 2] = iy + 1u;
+      dhs[i * 3 + 0] = h0; dhs[i * 3 + 1] = h1; dhs[i * 3 + 2] = h2;
+    }
+  }
+
+  // ---------------- per-pixel shading frame (fp32 contract; R-17)
+  float nx = nrm.x, ny = nrm.y, nz = nrm.z;
+  normalize3(nx, ny, nz);
+  const float sgn = copysignf(1.0f, nz);
+  const float oa = -1.0f / (sgn + nz);
+  const float ob = (nx * ny) * oa;
+  const float tx = 1.0f + sgn * ((nx * nx) * oa), ty = sgn * ob, tz = -(sgn * nx);
+  const float bx = ob, by = sgn + (ny * ny) * oa, bz = -ny;
+  float wix, wiy, wiz;
+  if (sc.view_kind == 0) { wix = sc.view[0] - pos.x; wiy = sc.view[1] - pos.y; wiz = sc.view[2] - pos.z; }
+  else { wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2]; }
+  normalize3(wix, wiy, wiz);
+  const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
+  const float iax = 1.0f / ax, iay = 1.0f / ay;
+  // radiance-path constants (tolerance path: fast intrinsics allowed)
+  const float ax2 = ax * ax, ay2 = ay * ay;
+  const float lam_i = smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wix, wiy, wiz, tx, ty, tz),
+                                   dot3(wix, wiy, wiz, bx, by, bz), ni);
+  // D_P / (4 n.wi) = C D(n) / (R N P 4 n.wi), D(n) = 1/(pi ax ay)  (Eq. 2-4, R-20)
+  const float dp_scale = __fdividef(1.0f, 3.14159265358979f * ax * ay * R * N * P);
+  const float rad_scale = __fdividef(dp_scale, 4.0f * ni);
+  float3 rgb = make_float3(0.0f, 0.0f, 0.0f);
+
+  for (int l = 0; l < L; ++l) {
+    const glint_light& lt = sc.lights[l];
+    // ---------------- S5: light direction d (unnormalised), activity, h, p
+    float dx, dy, dz;
+    if (lt.kind == 0) { dx = lt.pos_or_dir[0] - pos.x; dy = lt.pos_or_dir[1] - pos.y; dz = lt.pos_or_dir[2] - pos.z; }
+    else { dx = lt.pos_or_dir[0]; dy = lt.pos_or_dir[1]; dz = lt.pos_or_dir[2]; }
+    const float d2 = dot3(dx, dy, dz, dx, dy, dz);
+    const float nd = dot3(nx, ny, nz, dx, dy, dz);    // sign of n.wo
+    glint_debug_rec* rc = DEBUG ? rec + l : nullptr;
+    if (DEBUG) {
+      uint32_t* w = reinterpret_cast<uint32_t*>(rc);
+      for (int q = 0; q < (int)(sizeof(glint_debug_rec) / 4); ++q) w[q] = 0u;
+      rc->P = P; rc->r = r; rc->psi = psi;
+      for (int i = 0; i < 4; ++i) { rc->ls[i] = sl[i].ls; rc->lr[i] = sl[i].lr; rc->jo[i] = sl[i].jo; rc->w[i] = sl[i].w; rc->n[i] = n[i]; }
+      for (int q = 0; q < 12; ++q) { rc->lx[q] = (int32_t)dlx[q]; rc->ly[q] = (int32_t)dly[q]; }
+    }
+    if (!(ni > 0.0f && nd > 0.0f)) continue;   // light below the horizon (R-27)
+    if (DEBUG) rc->light_active = 1u;
+    // h = normalize(|d| wi + d)  (proportional to wi + wo, one division less)
+    const float dl = sqrtf(d2);
+    float hx_ = __fmaf_rn(dl, wix, dx), hy_ = __fmaf_rn(dl, wiy, dy), hz_ = __fmaf_rn(dl, wiz, dz);
+    normalize3(hx_, hy_, hz_);
+    const float hx = dot3(hx_, hy_, hz_, tx, ty, tz);
+    const float hy = dot3(hx_, hy_, hz_, bx, by, bz);
+    const float hz = dot3(hx_, hy_, hz_, nx, ny, nz);
+    // Eq. 4: p = R D(h)/D(n), GGX / Beckmann (R-19, R-22)
+    float ratio = 0.0f;
+    if (hz > 0.0f) {
+      const float X = hx * iax, Y = hy * iay;
+      const float s2 = X * X + Y * Y;
+      const float hz2 = hz * hz;
+      if (sc.ndf_kind == 0) {
+        const float q = s2 + hz2;
+        ratio = 1.0f / (q * q);
+      } else {
+        const float e2 = s2 / hz2;
+        ratio = exp2c(-(e2 * 0x1.715476p+0f)) / (hz2 * hz2);
+      }
+    }
+    float p = R * ratio;
+    if (p > 1.0f) { p = 1.0f; flags |= GLINT_FLAG_P_CLAMPED; }
+    if (!(p > 0.0f)) p = 0.0f;
+    // Eq. 14 angular grid (R-17); angular seeds pre-multiplied by C1
+    const float gxa = __fmaf_rn(hx, inv_beta, -0.5f), gya = __fmaf_rn(hy, inv_beta, -0.5f);
+    const float cxf = floorf(gxa), cyf = floorf(gya);
+    const float fxa = gxa - cxf, fya = gya - cyf;
+    const int cx0 = (int)cxf, cy0 = (int)cyf;
+    const float vj[4] = {(1.0f - fxa) * (1.0f - fya), fxa * (1.0f - fya), (1.0f - fxa) * fya, fxa * fya};
+    uint32_t kaC[4];
+#pragma unroll
+    for (int jn = 0; jn < 4; ++jn) {
+      const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
+      kaC[jn] = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU;
+    }
+    if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
+
+    // ---------------- S6 + S7 + S8: 48 gated draws, blended
+    const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
+    float C = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const Gate gt = gate_params(n[i], p, L2);
+      // gate (h >> 9) < T  <=>  h <= T*512 - 1; T = 0 wraps to "always" but its
+      // cap is forced to 0 so the count is 0 (same result, one compare)
+      const uint32_t G = (gt.T << 9) - 1u;
+      const float capk = gt.T ? gt.cap : 0.0f;
+      if (DEBUG) { rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap; }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int jn = 0; jn < 4; ++jn) {
+          uint32_t h = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
+          h ^= h >> 15;
+          h *= 0x846ca68bU;
+          h ^= h >> 16;                                  // = lowbias32_tail(hs + ka)
+          const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
+          const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
+          if (h <= G) acc = __fmaf_rn(vj[jn], c, acc);
+          if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = h; rc->count[i * 12 + k * 4 + jn] = (h <= G) ? c : 0.0f; }
+        }
+        C = __fmaf_rn(beta[i * 3 + k], acc, C);
+      }
+    }
+    if (DEBUG) { rc->C = C; rc->Dp = C * dp_scale; (void)dhs; }
+    // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
+    if (C > 0.0f) {
+      const float idl = __fdividef(1.0f, dl);
+      const float wox = dx * idl, woy = dy * idl, woz = dz * idl;
+      const float E = (lt.kind == 0) ? __fdividef(1.0f, d2) : 1.0f;
+      const float G2 = __fdividef(1.0f, 1.0f + lam_i + smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wox, woy, woz, tx, ty, tz),
+                                                                   dot3(wox, woy, woz, bx, by, bz), nd * idl));
+      const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
+      const float om = 1.0f - cih;
+      const float om2 = om * om;
+      const float om5 = om2 * om2 * om;
+      const float kk = G2 * C * rad_scale * E;
+      rgb.x += (sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk * lt.intensity[0];
+      rgb.y += (sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk * lt.intensity[1];
+      rgb.z += (sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk * lt.intensity[2];
+    }
+  }
+  if (DEBUG) for (int l = 0; l < L; ++l) rec[l].flags = flags;
+  __stcs(outp, make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(flags)));
+}
+
+// ---------------------------------------------------------------------------
+// The kernel: persistent blocks over 256-pixel tiles. TMA (contiguous
+// G-buffer, pitch == width): one thread issues the 5 bulk copies (5 x 4 KB)
+// of the block's next tile into the second buffer while the block shades the
+// current one (mbarrier-tracked, double-buffered); the block stays in step,
+// which keeps its warps in the same code (instruction-cache friendly).
+// Otherwise the planes are read directly.
+// ---------------------------------------------------------------------------
+template <bool DEBUG, bool TMA>
+__global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* sZ = reinterpret_cast<float*>(smem);
+  float2* sCS = reinterpret_cast<float2*>(smem + kSmemZ);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemZ + kSmemCS);
+  float4* tiles = reinterpret_cast<float4*>(smem + kSmemTables);
+  const int tid = threadIdx.x;
+  for (int i = tid; i < GLINT_ZQ; i += kBlock) sZ[i] = prm.ztab[i];
+  for (int i = tid; i < GLINT_NANG; i += kBlock) sCS[i] = prm.cstab[i];
+  if (TMA && tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
 
   const glint_scene& sc = prm.sc;
-  const int L = sc.n_lights;
   const int64_t n_pix = (int64_t)prm.width * prm.height;
+  const int64_t n_tiles = (n_pix + kBlock - 1) / kBlock;
   const float inv_beta = 1.0f / sc.beta;
   const uint32_t seed_h = lowbias32(sc.seed);
+  const bool flat_out = prm.out_pitch == prm.width;
 
-  for (int64_t idx = (int64_t)blockIdx.x * kBlock + threadIdx.x; idx < n_pix;
-       idx += (int64_t)gridDim.x * kBlock) {
-    const int y = (int)(idx / prm.width);
-    const int x = (int)(idx - (int64_t)y * prm.width);
-    const int64_t gi = (int64_t)y * prm.pitch + x;
-    // ---------------- S0: coalesced float4 loads (read-once, streaming)
-    const float4 duv = __ldcs(prm.duv + gi);
-    const float4 uvm = __ldcs(prm.uvm + gi);
-    const float4 nrm = __ldcs(prm.nrm + gi);
-    const float4 pos = __ldcs(prm.pos + gi);
-    const float4 mat = __ldcs(prm.mat + gi);
-    glint_debug_rec* rec = DEBUG ? prm.dbg + idx * L : nullptr;
+  auto issue = [&](int64_t t, int b) {   // one thread: 5 bulk copies of tile t into buffer b
+    const int64_t base = t * kBlock;
+    const int64_t cnt = (n_pix - base) < kBlock ? (n_pix - base) : kBlock;
+    const uint32_t bytes = (uint32_t)cnt * 16u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[b], 5u * bytes);
+    bulk_g2s(tiles + (b * 5 + 0) * kBlock, prm.duv + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 1) * kBlock, prm.uvm + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 2) * kBlock, prm.nrm + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 3) * kBlock, prm.pos + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 4) * kBlock, prm.mat + base, bytes, &bars[b]);
+  };
 
-    uint32_t flags = 0;
-    float3 rgb = make_float3(0.0f, 0.0f, 0.0f);
-    const uint32_t meta = __float_as_uint(uvm.w);
-    const float u = uvm.x, v = uvm.y;
-    bool ok = (meta & 1u) != 0;
-    if (!ok) flags = GLINT_FLAG_INVALID;
-    if (ok && !(fabsf(u) <= 0x1p24f && fabsf(v) <= 0x1p24f)) {
-      flags = GLINT_FLAG_INVALID | GLINT_FLAG_UV_RANGE;
-      ok = false;
+  int64_t t = blockIdx.x;
+  if (TMA && tid == 0 && t < n_tiles) issue(t, 0);
+  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (TMA) {
+      __syncthreads();   // the whole block is done reading buffer b^1 (iteration it-1)
+      if (tid == 0 && t + gridDim.x < n_tiles) issue(t + gridDim.x, b ^ 1);
+      mbar_wait(&bars[b], (uint32_t)(it >> 1) & 1u);
     }
-    // ---------------- S1: footprint (R-7, R-8)
-    float P = 0.0f, r = 0.0f, psi = 0.0f;
-    if (ok) {
-      const float dudx = duv.x, dvdx = duv.y, dudy = duv.z, dvdy = duv.w;
-      const float det = dudx * dvdy - dvdx * dudy;
-      const float a = dudx * dudx + dudy * dudy;
-      const float b = dudx * dvdx + dudy * dvdy;
-      const float c = dvdx * dvdx + dvdy * dvdy;
-      const float hm = 0.5f * (a - c);
-      const float disc = sqrtf(hm * hm + b * b);
-      const float lam = 0.5f * (a + c) + disc;
-      P = fabsf(det);
-      r = lam / P;
-      const float at = atan2_turns(2.0f * b, a - c);
-      psi = at < 0.0f ? at + 1.0f : at;
-      if (psi >= 1.0f) psi = 0.0f;
-      if (!(P >= 0x1p-64f && P < 0x1p64f)) {
-        flags = GLINT_FLAG_DEGENERATE;
-        ok = false;
+    const int64_t idx = t * kBlock + tid;
+    if (idx >= n_pix) continue;
+    float4 duv, uvm, nrm, pos, mat;
+    int64_t oi = idx;
+    if (TMA) {
+      const float4* tb = tiles + b * 5 * kBlock + tid;
+      duv = tb[0]; uvm = tb[kBlock]; nrm = tb[2 * kBlock]; pos = tb[3 * kBlock]; mat = tb[4 * kBlock];
+      if (!flat_out) {
+        const uint32_t y = (uint32_t)idx / (uint32_t)prm.width;
+        oi = (int64_t)y * prm.out_pitch + ((uint32_t)idx - y * (uint32_t)prm.width);
       }
+    } else {
+      const uint32_t y = (uint32_t)idx / (uint32_t)prm.width;
+      const uint32_t x = (uint32_t)idx - y * (uint32_t)prm.width;
+      const int64_t gi = (int64_t)y * prm.pitch + x;
+      duv = __ldcs(prm.duv + gi); uvm = __ldcs(prm.uvm + gi); nrm = __ldcs(prm.nrm + gi);
+      pos = __ldcs(prm.pos + gi); mat = __ldcs(prm.mat + gi);
+      oi = (int64_t)y * prm.out_pitch + x;
     }
-    if (!ok) {
-      prm.out[(int64_t)y * prm.out_pitch + x] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(flags));
-      if (DEBUG) {
-        for (int l = 0; l < L; ++l) {
-          uint32_t* w = reinterpret_cast<uint32_t*>(rec + l);
-          for (int q = 0; q < (int)(sizeof(glint_debug_rec) / 4); ++q) w[q] = 0u;
-          rec[l].flags = flags;
-        }
-      }
-      continue;
-    }
-
-    // ---------------- S2: 4 grids + distribution weights, n_i = w_i N 2^ls
-    Slot sl[4];
-    lattice(P, r, psi, sc.max_ratio_level, sl, flags);
-    const float ax = mat.x, ay = mat.y, N = mat.z, R = mat.w;
-    float n[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) n[i] = sl[i].w * (N * pow2i(sl[i].ls));
-
-    // ---------------- S3 + S4a: grid transform, simplex, spatial seeds
-    const uint32_t so = lowbias32(__float_as_uint(uvm.z) ^ seed_h);
-    uint32_t hsx[12];   // lowbias32 spatial hash, pre-xorshifted by 16 for the draw hash
-    float beta[12];
-    uint32_t dlx[DEBUG ? 12 : 1], dly[DEBUG ? 12 : 1];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float2 cs = sCS[sl[i].jo << (8 - sl[i].lr)];
-      const float xr = __fmaf_rn(cs.x, u, cs.y * v);
-      const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
-      const float gx = xr * pow2half(-(sl[i].ls + sl[i].lr));
-      const float gy = yr * pow2half(sl[i].lr - sl[i].ls);
-      const float xs = gx + 0.5f * gy;
-      const float fxs = floorf(xs), fys = floorf(gy);
-      const float fx = xs - fxs, fy = gy - fys;
-      const uint32_t ix = (uint32_t)(long long)fxs, iy = (uint32_t)(long long)fys;
-      const bool lower = fx >= fy;
-      // vertices: (ix,iy), lower ? (ix+1,iy) : (ix,iy+1), (ix+1,iy+1)
-      const uint32_t lx1 = lower ? ix + 1u : ix, ly1 = lower ? iy : iy + 1u;
-      beta[i * 3 + 0] = 1.0f - (lower ? fx : fy);
-      beta[i * 3 + 1] = lower ? fx - fy : fy - fx;
-      beta[i * 3 + 2] = lower ? fy : fx;
-      const uint32_t key = ((uint32_t)sl[i].ls & 511u) | ((uint32_t)sl[i].lr << 9) | ((uint32_t)sl[i].jo << 13);
-      const uint32_t g = lowbias32(so ^ key);
-      const uint32_t lxs[3] = {ix, lx1, ix + 1u}, lys[3] = {iy, ly1, iy + 1u};
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const uint32_t hs = lowbias32(g ^ (lxs[k] * 0x8da6b343U + lys[k] * 0xd8163841U));
-        hsx[i * 3 + k] = hs ^ (hs >> 16);
-        if (DEBUG) { dlx[i * 3 + k] = lxs[k]; dly[i * 3 + k] = lys[k]; }
-      }
-    }
-
-    // ---------------- per-pixel shading frame (fp32 contract; R-17)
-    float nx = nrm.x, ny = nrm.y, nz = nrm.z;
-    normalize3(nx, ny, nz);
-    const float sgn = copysignf(1.0f, nz);
-    const float oa = -1.0f / (sgn + nz);
-    const float ob = (nx * ny) * oa;
-    const float tx = 1.0f + sgn * ((nx * nx) * oa), ty = sgn * ob, tz = -(sgn * nx);
-    const float bx = ob, by = sgn + (ny * ny) * oa, bz = -ny;
-    float wix, wiy, wiz;
-    if (sc.view_kind == 0) { wix = sc.view[0] - pos.x; wiy = sc.view[1] - pos.y; wiz = sc.view[2] - pos.z; }
-    else { wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2]; }
-    normalize3(wix, wiy, wiz);
-    const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
-    const float wilx = dot3(wix, wiy, wiz, tx, ty, tz), wily = dot3(wix, wiy, wiz, bx, by, bz);
-    const float ax2 = ax * ax, ay2 = ay * ay;
-    const float lam_i = smith_lambda(sc.ndf_kind, ax2, ay2, wilx, wily, ni);
-    // D_P = C * Dn / (R N P) with D(n) = 1 / (pi ax ay)  (Eq. 3-4, R-20)
-    const float dp_scale = 1.0f / (3.14159265358979f * ax * ay * R * N * P);
-
-    for (int l = 0; l < L; ++l) {
-      const glint_light& lt = sc.lights[l];
-      // ---------------- S5: light direction, activity, h, p, angular nodes
-      float wox, woy, woz;
-      if (lt.kind == 0) { wox = lt.pos_or_dir[0] - pos.x; woy = lt.pos_or_dir[1] - pos.y; woz = lt.pos_or_dir[2] - pos.z; }
-      else { wox = lt.pos_or_dir[0]; woy = lt.pos_or_dir[1]; woz = lt.pos_or_dir[2]; }
-      const float d2 = dot3(wox, woy, woz, wox, woy, woz);
-      normalize3(wox, woy, woz);
-      const float no = dot3(nx, ny, nz, wox, woy, woz);
-      glint_debug_rec* rc = DEBUG ? rec + l : nullptr;
-      if (DEBUG) {
-        uint32_t* w = reinterpret_cast<uint32_t*>(rc);
-        for (int q = 0; q < (int)(sizeof(glint_debug_rec) / 4); ++q) w[q] = 0u;
-        rc->P = P; rc->r = r; rc->psi = psi;
-        for (int i = 0; i < 4; ++i) { rc->ls[i] = sl[i].ls; rc->lr[i] = sl[i].lr; rc->jo[i] = sl[i].jo; rc->w[i] = sl[i].w; rc->n[i] = n[i]; }
-        for (int q = 0; q < 12; ++q) { rc->lx[q] = (int32_t)dlx[q]; rc->ly[q] = (int32_t)dly[q]; }
-      }
-      if (!(ni > 0.0f && no > 0.0f)) continue;   // light below the horizon (R-27)
-      if (DEBUG) rc->light_active = 1u;
-      float hx_ = wix + wox, hy_ = wiy + woy, hz_ = wiz + woz;
-      normalize3(hx_, hy_, hz_);
-      const float hx = dot3(hx_, hy_, hz_, tx, ty, tz);
-      const float hy = dot3(hx_, hy_, hz_, bx, by, bz);
-      const float hz = dot3(hx_, hy_, hz_, nx, ny, nz);
-      // Eq. 4: p = R D(h)/D(n), GGX / Beckmann (R-19, R-22)
-      float ratio = 0.0f;
-      if (hz > 0.0f) {
-        const float X = hx / ax, Y = hy / ay;
-        const float s2 = X * X + Y * Y;
-        const float hz2 = hz * hz;
-        if (sc.ndf_kind == 0) {
-          const float q = s2 + hz2;
-          ratio = 1.0f / (q * q);
-        } else {
-          const float e2 = s2 / hz2;
-          ratio = exp2c(-(e2 * 0x1.715476p+0f)) / (hz2 * hz2);
-        }
-      }
-      float p = R * ratio;
-      if (p > 1.0f) { p = 1.0f; flags |= GLINT_FLAG_P_CLAMPED; }
-      if (!(p > 0.0f)) p = 0.0f;
-      // Eq. 14 angular grid (R-17)
-      const float gxa = __fmaf_rn(hx, inv_beta, -0.5f), gya = __fmaf_rn(hy, inv_beta, -0.5f);
-      const float cxf = floorf(gxa), cyf = floorf(gya);
-      const float fxa = gxa - cxf, fya = gya - cyf;
-      const int cx0 = (int)cxf, cy0 = (int)cyf;
-      const float vj[4] = {(1.0f - fxa) * (1.0f - fya), fxa * (1.0f - fya), (1.0f - fxa) * fya, fxa * fya};
-      uint32_t kax[4];
-#pragma unroll
-      for (int jn = 0; jn < 4; ++jn) {
-        const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
-        const uint32_t ka = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
-        kax[jn] = ka ^ (ka >> 16);
-      }
-      if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
-
-      // ---------------- S6 + S7 + S8: 48 gated draws, blended
-      const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
-      float C = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const Gate gt = gate_params(n[i], p, L2);
-        if (DEBUG) { rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap; }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          float cik = 0.0f;
-#pragma unroll
-          for (int jn = 0; jn < 4; ++jn) {
-            const uint32_t h = lowbias32_tail(hsx[i * 3 + k] ^ kax[jn]);
-            const float c = gated_count(h, gt, sZ);
-            cik = __fmaf_rn(vj[jn], c, cik);
-            if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = h; rc->count[i * 12 + k * 4 + jn] = c; }
-          }
-          C = __fmaf_rn(beta[i * 3 + k], cik, C);
-        }
-      }
-      // ---------------- S8/S9: D_P and radiance (Eq. 1-3)
-      const float Dp = C * dp_scale;
-      if (DEBUG) { rc->C = C; rc->Dp = Dp; }
-      if (C > 0.0f) {
-        const float E = (lt.kind == 0) ? 1.0f / d2 : 1.0f;
-        const float wolx = dot3(wox, woy, woz, tx, ty, tz), woly = dot3(wox, woy, woz, bx, by, bz);
-        const float G2 = 1.0f / (1.0f + lam_i + smith_lambda(sc.ndf_kind, ax2, ay2, wolx, woly, no));
-        const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
-        const float om = 1.0f - cih;
-        const float om2 = om * om;
-        const float om5 = om2 * om2 * om;
-        const float k = G2 * Dp * E / (4.0f * ni);
-        rgb.x += (sc.f0[0] + (1.0f - sc.f0[0]) * om5) * k * lt.intensity[0];
-        rgb.y += (sc.f0[1] + (1.0f - sc.f0[1]) * om5) * k * lt.intensity[1];
-        rgb.z += (sc.f0[2] + (1.0f - sc.f0[2]) * om5) * k * lt.intensity[2];
-      }
-    }
-    if (DEBUG) for (int l = 0; l < L; ++l) rec[l].flags = flags;
-    __stcs(prm.out + (int64_t)y * prm.out_pitch + x, make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(flags)));
+    shade_pixel<DEBUG>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm, pos,
+                       mat, seed_h, inv_beta);
   }
 }
 
-template __global__ void glint_eval_kernel<false>(const KParams);
-template __global__ void glint_eval_kernel<true>(const KParams);
-
-cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream) {
-  if (debug)
-    glint_eval_kernel<true><<<grid, kBlock, 0, stream>>>(prm);
-  else
-    glint_eval_kernel<false><<<grid, kBlock, 0, stream>>>(prm);
+template <bool DEBUG, bool TMA>
+static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream) {
+  const size_t smem = TMA ? kSmemTma : kSmemTables;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  glint_eval_kernel<DEBUG, TMA><<<grid, kBlock, smem, stream>>>(prm);
   return cudaGetLastError();
 }
 
+cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream) {
+  const bool tma = (prm.pitch == prm.width) && (((uintptr_t)prm.duv | (uintptr_t)prm.uvm | (uintptr_t)prm.nrm |
+                                                  (uintptr_t)prm.pos | (uintptr_t)prm.mat) % 16 == 0);
+  if (debug) return tma ? launch_t<true, true>(prm, grid, stream) : launch_t<true, false>(prm, grid, stream);
+  return tma ? launch_t<false, true>(prm, grid, stream) : launch_t<false, false>(prm, grid, stream);
+}
+
 cudaError_t occupancy_blocks_per_sm(int* out) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false>, kBlock, 0);
+  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kSmemTma);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true>, kBlock, kSmemTma);
 }
 
 }  // namespace glint

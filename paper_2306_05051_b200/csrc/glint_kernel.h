@@ -8,6 +8,11 @@
 namespace glint {
 
 constexpr int kBlock = 256;
+constexpr int kMinBlocks = 3;   // resident blocks per SM the register budget targets
+constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
+constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
+constexpr size_t kSmemTables = kSmemZ + kSmemCS + 128;          // + 2 mbarriers per warp (8 warps)
+constexpr size_t kSmemTma = kSmemTables + 2 * 5 * kBlock * 16;  // + per warp 2 x 5 planes x 32 float4
 
 struct KParams {
   const float4* duv;
