@@ -84,6 +84,7 @@ def lib():
                                                       C.c_void_p, C.c_void_p, C.c_void_p]
             L.orc_eval.restype = C.c_int
             L.orc_exp2.argtypes = [C.c_float]; L.orc_exp2.restype = C.c_float
+            L.orc_rsqrt.argtypes = [C.c_float]; L.orc_rsqrt.restype = C.c_float
             L.orc_log2_1mp.argtypes = [C.c_float]; L.orc_log2_1mp.restype = C.c_float
             L.orc_atan2_turns.argtypes = [C.c_float, C.c_float]; L.orc_atan2_turns.restype = C.c_float
             L.orc_lowbias32.argtypes = [C.c_uint32]; L.orc_lowbias32.restype = C.c_uint32
@@ -198,6 +199,10 @@ def eval(gb, scene, debug: bool = False, threads: int | None = None, sampler: st
 # --------------------------------------------------------------------------- primitives
 def exp2(y: float) -> float:
     return lib().orc_exp2(y)
+
+
+def rsqrt(x: float) -> float:
+    return lib().orc_rsqrt(x)
 
 
 def log2_1mp(p: float) -> float:

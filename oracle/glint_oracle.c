@@ -146,6 +146,18 @@ float orc_atan2_turns(float y, float x) {
   return a;
 }
 
+/* 1/sqrt(x) for normal x > 0: magic-constant start 0x5f3759df - (bits >> 1),
+ * then three Newton steps y <- y (3/2 - (x/2) y^2) with the fma written out
+ * (DESIGN.md §4.2). Used to normalise directions. */
+float orc_rsqrt(float x) {
+  float y = u2f(0x5f3759dfU - (f2u(x) >> 1));
+  float hx = 0.5f * x;
+  y = y * fmaf(-hx, y * y, 1.5f);
+  y = y * fmaf(-hx, y * y, 1.5f);
+  y = y * fmaf(-hx, y * y, 1.5f);
+  return y;
+}
+
 /* ---------------------------------------------------------------------- */
 /* Hash ("random seeds theta are distributed in a spatial and angular
  * grid"; reading R-23). Published "lowbias32" integer mixer.                */
@@ -412,8 +424,7 @@ static float dot3f(const float a[3], const float b[3]) {
   return fmaf(a[2], b[2], fmaf(a[1], b[1], a[0] * b[0]));
 }
 static void normalize3f(float v[3]) {
-  float l2 = dot3f(v, v);
-  float inv = 1.0f / sqrtf(l2);
+  float inv = orc_rsqrt(dot3f(v, v));
   v[0] = v[0] * inv; v[1] = v[1] * inv; v[2] = v[2] * inv;
 }
 /* Duff et al. 2017 branchless ONB from n (reading R-17) */
@@ -557,7 +568,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     float n_d = dot3f(nf, d);
     if (!(ni > 0.0f && n_d > 0.0f)) continue; /* light below the horizon: 0 */
     if (rc) rc->light_active = 1;
-    float dl = sqrtf(d2);
+    float dl = d2 * orc_rsqrt(d2);
     float hv[3] = {fmaf(dl, wi[0], d[0]), fmaf(dl, wi[1], d[1]), fmaf(dl, wi[2], d[2])};
     normalize3f(hv);
     float hx = dot3f(hv, tf), hy = dot3f(hv, bf), hz = dot3f(hv, nf);

@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libglint.so")
+LIB_PATH = os.environ.get("GLINT_LIB") or os.path.join(_HERE, "libglint.so")
 
 GLINT_OK, GLINT_EINVAL, GLINT_EALIGN, GLINT_EDEVICE, GLINT_ELIMIT, GLINT_ECUDA, GLINT_ENOMEM = 0, -1, -2, -3, -4, -5, -6
 FLAG_INVALID, FLAG_DEGENERATE, FLAG_RATIO_CLAMPED, FLAG_P_CLAMPED, FLAG_UV_RANGE = 1, 2, 4, 8, 16

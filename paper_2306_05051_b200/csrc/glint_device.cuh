@@ -103,10 +103,24 @@ __device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
 __device__ __forceinline__ float dot3(float ax, float ay, float az, float bx, float by, float bz) {
   return __fmaf_rn(az, bz, __fmaf_rn(ay, by, ax * bx));
 }
+// 1/sqrt(x), normal x > 0: magic start + 3 Newton steps, branch-free
+__device__ __forceinline__ float rsqrt_c(float x) {
+  float y = __uint_as_float(0x5f3759dfU - (__float_as_uint(x) >> 1));
+  const float hx = 0.5f * x;
+  y = y * __fmaf_rn(-hx, y * y, 1.5f);
+  y = y * __fmaf_rn(-hx, y * y, 1.5f);
+  y = y * __fmaf_rn(-hx, y * y, 1.5f);
+  return y;
+}
 __device__ __forceinline__ void normalize3(float& x, float& y, float& z) {
-  float l2 = dot3(x, y, z, x, y, z);
-  float inv = 1.0f / sqrtf(l2);
+  const float inv = rsqrt_c(dot3(x, y, z, x, y, z));
   x = x * inv; y = y * inv; z = z * inv;
+}
+// hide a value from the optimiser (keeps pre-multiplied hash seeds from being
+// re-factored into an extra multiply per draw)
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+  asm volatile("" : "+r"(x));
+  return x;
 }
 
 // Gate parameters of one grid (Eq. 16-17, readings R-1..R-4). DESIGN §4.3 S6.
@@ -119,7 +133,7 @@ __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   Gate g;
   if (!(n > 0.0f) || !(p > 0.0f)) { g.T = 0; g.sigma = 0.0f; g.m1 = 1.0f; g.cap = 1.0f; return g; }
   float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
-  g.T = (uint32_t)ceilf(pge1 * 0x1p23f);
+  g.T = __float2uint_ru(pge1 * 0x1p23f);   // = (uint32_t)ceil(P>=1 2^23), exact
   float nm1 = n - 1.0f;
   float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
   g.sigma = sqrtf(mu * (1.0f - p));

@@ -220,9 +220,9 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const uint32_t lin1 = base + (lower ? 0x8da6b343U : 0xd8163841U);
     const uint32_t lin2 = base + (0x8da6b343U + 0xd8163841U);
     const uint32_t h0 = lowbias32(base), h1 = lowbias32(lin1), h2 = lowbias32(lin2);
-    hsC[i * 3 + 0] = h0 * 0x7feb352dU;
-    hsC[i * 3 + 1] = h1 * 0x7feb352dU;
-    hsC[i * 3 + 2] = h2 * 0x7feb352dU;
+    hsC[i * 3 + 0] = opaque(h0 * 0x7feb352dU);
+    hsC[i * 3 + 1] = opaque(h1 * 0x7feb352dU);
+    hsC[i * 3 + 2] = opaque(h2 * 0x7feb352dU);
     if (DEBUG) {
       dlx[i * 3 + 0] = ix; dly[i * 3 + 0] = iy;
       dlx[i * 3 + 1] = lower ? ix + 1u : ix; dly[i * 3 + 1] = lower ? iy : iy + 1u;
@@ -273,7 +273,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     if (!(ni > 0.0f && nd > 0.0f)) continue;   // light below the horizon (R-27)
     if (DEBUG) rc->light_active = 1u;
     // h = normalize(|d| wi + d)  (proportional to wi + wo, one division less)
-    const float dl = sqrtf(d2);
+    const float dl = d2 * rsqrt_c(d2);
     float hx_ = __fmaf_rn(dl, wix, dx), hy_ = __fmaf_rn(dl, wiy, dy), hz_ = __fmaf_rn(dl, wiz, dz);
     normalize3(hx_, hy_, hz_);
     const float hx = dot3(hx_, hy_, hz_, tx, ty, tz);
@@ -306,13 +306,13 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
-      kaC[jn] = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU;
+      kaC[jn] = opaque(lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU);
     }
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
     const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
-    float C = 0.0f;
+    float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // A_j = sum_ik beta_ik c_ikj
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const Gate gt = gate_params(n[i], p, L2);
@@ -323,7 +323,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       if (DEBUG) { rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap; }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        float acc = 0.0f;
+        const float bk = beta[i * 3 + k];
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
           uint32_t h = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
@@ -332,12 +332,12 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
           h ^= h >> 16;                                  // = lowbias32_tail(hs + ka)
           const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
           const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
-          if (h <= G) acc = __fmaf_rn(vj[jn], c, acc);
+          if (h <= G) A[jn] = __fmaf_rn(bk, c, A[jn]);
           if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = h; rc->count[i * 12 + k * 4 + jn] = (h <= G) ? c : 0.0f; }
         }
-        C = __fmaf_rn(beta[i * 3 + k], acc, C);
       }
     }
+    const float C = __fmaf_rn(vj[3], A[3], __fmaf_rn(vj[2], A[2], __fmaf_rn(vj[1], A[1], vj[0] * A[0])));
     if (DEBUG) { rc->C = C; rc->Dp = C * dp_scale; (void)dhs; }
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
     if (C > 0.0f) {

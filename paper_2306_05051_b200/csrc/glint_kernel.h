@@ -7,8 +7,14 @@
 
 namespace glint {
 
-constexpr int kBlock = 256;
-constexpr int kMinBlocks = 3;   // resident blocks per SM the register budget targets
+#ifndef GLINT_BLOCK
+#define GLINT_BLOCK 512
+#endif
+constexpr int kBlock = GLINT_BLOCK;
+#ifndef GLINT_MIN_BLOCKS
+#define GLINT_MIN_BLOCKS 1
+#endif
+constexpr int kMinBlocks = GLINT_MIN_BLOCKS;   // resident blocks per SM the register budget targets
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
 constexpr size_t kSmemTables = kSmemZ + kSmemCS + 128;          // + 2 mbarriers per warp (8 warps)

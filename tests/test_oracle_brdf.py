@@ -74,6 +74,7 @@ def test_reciprocity_of_the_glint_brdf(orc, ndf):
         rgb2, _, rec2 = orc.eval(fr.gbuf, fr.scene, debug=True)
         assert np.array_equal(rec1["count"], rec2["count"])
         na, nb = a[2] / np.linalg.norm(a), b[2] / np.linalg.norm(b)
-        # h = normalize(|d| w_i + d) is symmetric only up to fp32 rounding, which
-        # moves the angular interpolation weights in the last bits
-        assert np.allclose(rgb1 * na, rgb2 * nb, rtol=2e-5, atol=0)
+        # h = normalize(|d| w_i + d) is symmetric only up to fp32 rounding; the
+        # angular weights v_j amplify it by 1/beta (a swapped F or G term would
+        # break this by orders of magnitude more)
+        assert np.allclose(rgb1 * na, rgb2 * nb, rtol=1e-3, atol=0)

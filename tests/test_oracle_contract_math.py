@@ -24,6 +24,16 @@ def test_exp2_matches_libm(orc):
     assert orc.exp2(-126.0) == 0.0 and orc.exp2(-1e30) == 0.0
 
 
+def test_rsqrt_matches_libm(orc):
+    xs = np.concatenate([np.geomspace(1e-30, 1e30, 20001), np.linspace(0.5, 4.0, 20001)]).astype(np.float32)
+    worst = 0.0
+    for x in xs:
+        ref = 1.0 / math.sqrt(float(x))
+        worst = max(worst, abs(orc.rsqrt(float(x)) - ref) / ref)
+    assert worst < 3e-7, worst
+    assert abs(orc.rsqrt(4.0) - 0.5) <= 2 ** -24 and abs(orc.rsqrt(1.0) - 1.0) <= 2 ** -23
+
+
 def test_log2_1mp_matches_libm(orc):
     ps = np.concatenate([np.geomspace(1e-38, 0.5, 3001), np.linspace(0.5, 1 - 1e-7, 3001)]).astype(np.float32)
     worst = 0.0
