@@ -171,8 +171,8 @@ uint32_t orc_lowbias32(uint32_t x) {
   return x;
 }
 
-/* the last four steps of lowbias32; the per-draw hash is tail(hs + ka) of
- * the spatial seed hs and the angular seed ka (both full lowbias32 outputs) */
+/* the last four steps of lowbias32; the per-draw hash is h = tail(hs + ka)
+ * of the spatial seed hs and the angular seed ka (both full lowbias32 outputs) */
 uint32_t orc_lowbias32_tail(uint32_t x) {
   x *= 0x7feb352dU;
   x ^= x >> 15;
@@ -354,8 +354,9 @@ void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]) 
 /* ---------------------------------------------------------------------- */
 /* S6  Gated Gaussian binomial (Eq. 16-18, readings R-1..R-4):
  * P>=1 = 1 - (1-p)^n; mu = (n-1)p, sigma = sqrt((n-1)p(1-p)); gate succeeds
- * iff theta0 < P>=1 with theta0 = (h >> 9) 2^-23, i.e. (h >> 9) < T where
- * T = ceil(P>=1 2^23); z = Z[(h >> 2) & 4095] (bits 2..13);
+ * iff theta0 < P>=1 with theta0 = (y >> 9) 2^-23, i.e. (y >> 9) < T, where
+ * y = h ^ (h >> 16) is the hash before its final xor-shift (the same top 16
+ * bits as h) and T = ceil(P>=1 2^23); z = Z[(h >> 2) & 4095] (bits 2..13);
  * count = floor(clamp(1 + mu + sigma z, 1, ceil(n))) (reading R-3).         */
 /* ---------------------------------------------------------------------- */
 void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap) {
@@ -370,14 +371,16 @@ void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, flo
   *T = (uint32_t)ceilf(Pge1 * 0x1p23f);
   float nm1 = n - 1.0f;
   float mu = nm1 > 0.0f ? nm1 * p : 0.0f; /* Eq. 17 (R-4: n < 1 -> mu = 0) */
-  *sigma = sqrtf(mu * (1.0f - p));
+  float var = mu * (1.0f - p);
+  *sigma = var > 0.0f ? var * orc_rsqrt(var) : 0.0f; /* sqrt via the contract rsqrt */
   *m1 = 1.0f + mu;
   *cap = ceilf(n);
 }
 
 float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap) {
   orc_init();
-  if (!((h >> 9) < T)) return 0.0f;               /* H(P>=1 - theta0) gate, R-1 */
+  uint32_t y = h ^ (h >> 16);                     /* undo the final xor-shift */
+  if (!((y >> 9) < T)) return 0.0f;               /* H(P>=1 - theta0) gate, R-1 */
   float z = g_z[(h >> 2) & (ORC_ZQ - 1)];         /* N(theta1) via quantile table, R-2 */
   float x = fmaf(sigma, z, m1);                   /* 1 + N(theta1; mu, sigma) */
   x = x < 1.0f ? 1.0f : x;                        /* R-3 clamp */

@@ -57,10 +57,13 @@ def gated_pmf_analytic(n: float, p: float, kmax: int | None = None) -> np.ndarra
 def gated_pmf_enumerated(n: float, p: float):
     """Exact law of the contract's gated draw assuming an ideal hash: P(gate) =
     T / 2^23 and the count given the gate is a function of the quantile cell
-    q = (h >> 2) & 4095 only (theta0 = (h >> 9) 2^-23 and z = Z[q]; the gate's
-    dependence on the 5 shared bits 9..13 is below 2^-18 and ignored here). Evaluated through
+    q = (h >> 2) & 4095 only (theta0 = (y >> 9) 2^-23 with y = h ^ (h >> 16), and
+    z = Z[q]; the residual gate/quantile dependence is below 2^-18 and ignored
+    here). Evaluated through
     the C oracle's own gate_params / gated_count for every q."""
     T, s, m1, cap = gate_params(n, p)
+    # h = q << 2 has y = h (bits >= 16 are zero), y >> 9 < 2^7 <= T for T >= 128;
+    # for tiny T pick the h with the same quantile cell and y >> 9 = 0
     counts = np.array([gated_count(q << 2, T, s, m1, cap) if T > 0 else 0 for q in range(ZQ)])
     kmax = int(max(cap, 1))
     pmf = np.zeros(kmax + 1)

@@ -22,7 +22,8 @@ __device__ __forceinline__ float pow2half(int e) {
 
 // exp2c(y), y <= 0 (Eq. 16 (1-p)^n and the Beckmann exponential). DESIGN §4.2.
 __device__ __forceinline__ float exp2c(float y) {
-  if (!(y >= -125.0f)) return 0.0f;
+  const bool under = !(y >= -125.0f);   // -> 0 (select, branch-free)
+  y = under ? 0.0f : y;
   float k = floorf(y + 0.5f);
   float f = y - k;
   float q = 0x1.ffcbfcp-17f;
@@ -33,7 +34,10 @@ __device__ __forceinline__ float exp2c(float y) {
   q = __fmaf_rn(q, f, 0x1.ebfbe0p-3f);
   q = __fmaf_rn(q, f, 0x1.62e430p-1f);
   q = __fmaf_rn(q, f, 1.0f);
-  return q * pow2i((int)k);
+  // 2^k for integer-valued k in [-125, 0] without a float->int convert: the
+  // low bits of k + (2^23 + 127) are k + 127
+  const float p2 = __uint_as_float(__float_as_uint(k + 8388735.0f) << 23);
+  return under ? 0.0f : q * p2;
 }
 
 // s * atanh(s)/s series to s^15 (Horner in s^2)
@@ -72,8 +76,10 @@ __device__ __forceinline__ float atan2_turns(float y, float x) {
   float mn = ax > ay ? ay : ax;
   if (mx == 0.0f) return 0.0f;
   float t = mn / mx;
-  float base = 0.0f;
-  if (t > 0x1.a8279ap-2f) { t = (t - 1.0f) / (t + 1.0f); base = 0.125f; }
+  const bool red = t > 0x1.a8279ap-2f;   // reduce by 1/8 turn (select, branch-free)
+  const float tr = (t - 1.0f) / (t + 1.0f);
+  t = red ? tr : t;
+  const float base = red ? 0.125f : 0.0f;
   float z = t * t;
   float q = 0x1.32c69ep-7f;
   q = __fmaf_rn(q, z, -0x1.5bade6p-7f);
@@ -130,15 +136,19 @@ struct Gate {
 };
 __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   // L2 = log2(1 - p) for p in (0,1), precomputed once per (pixel, light)
+  // branch-free: all candidates computed, selected
   Gate g;
-  if (!(n > 0.0f) || !(p > 0.0f)) { g.T = 0; g.sigma = 0.0f; g.m1 = 1.0f; g.cap = 1.0f; return g; }
-  float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
-  g.T = __float2uint_ru(pge1 * 0x1p23f);   // = (uint32_t)ceil(P>=1 2^23), exact
-  float nm1 = n - 1.0f;
-  float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
-  g.sigma = sqrtf(mu * (1.0f - p));
-  g.m1 = 1.0f + mu;
-  g.cap = ceilf(n);
+  const bool none = !(n > 0.0f) || !(p > 0.0f);
+  const float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
+  const uint32_t T = __float2uint_ru(pge1 * 0x1p23f);   // = (uint32_t)ceil(P>=1 2^23), exact
+  const float nm1 = n - 1.0f;
+  const float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
+  const float var = mu * (1.0f - p);
+  const float sg = var > 0.0f ? var * rsqrt_c(var) : 0.0f;   // sqrt via the contract rsqrt
+  g.T = none ? 0u : T;
+  g.sigma = none ? 0.0f : sg;
+  g.m1 = none ? 1.0f : 1.0f + mu;
+  g.cap = none ? 1.0f : ceilf(n);
   return g;
 }
 

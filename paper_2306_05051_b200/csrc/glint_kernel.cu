@@ -316,7 +316,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const Gate gt = gate_params(n[i], p, L2);
-      // gate (h >> 9) < T  <=>  h <= T*512 - 1; T = 0 wraps to "always" but its
+      // gate (y >> 9) < T  <=>  y <= T*512 - 1; T = 0 wraps to "always" but its
       // cap is forced to 0 so the count is 0 (same result, one compare)
       const uint32_t G = (gt.T << 9) - 1u;
       const float capk = gt.T ? gt.cap : 0.0f;
@@ -326,14 +326,14 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         const float bk = beta[i * 3 + k];
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
-          uint32_t h = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
-          h ^= h >> 15;
-          h *= 0x846ca68bU;
-          h ^= h >> 16;                                  // = lowbias32_tail(hs + ka)
-          const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
+          uint32_t y = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
+          y ^= y >> 15;
+          y *= 0x846ca68bU;                              // y: gate bits 9..31
+          const uint32_t s16 = y >> 16;                  // h = y ^ (y >> 16): quantile bits 2..13
+          const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
           const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
-          if (h <= G) A[jn] = __fmaf_rn(bk, c, A[jn]);
-          if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = h; rc->count[i * 12 + k * 4 + jn] = (h <= G) ? c : 0.0f; }
+          if (y <= G) A[jn] = __fmaf_rn(bk, c, A[jn]);
+          if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = y ^ s16; rc->count[i * 12 + k * 4 + jn] = (y <= G) ? c : 0.0f; }
         }
       }
     }

@@ -118,3 +118,34 @@ def test_orientation_table(orc):
     m = np.arange(256)
     assert np.array_equal(orc.costable(), np.cos(m * np.pi / 256).astype(np.float32))
     assert np.array_equal(orc.sintable(), np.sin(m * np.pi / 256).astype(np.float32))
+
+
+
+def test_draw_hash_decorrelates_angular_nodes(orc):
+    """The 4 angular draws of one texel hash hs + ka_j with fixed offsets
+    ka_j - ka_0 (reading R-23): output bits of tail(x) and tail(x + delta) must
+    differ with probability ~1/2 (no correlation between the nodes' draws), and
+    (gate bucket, quantile bucket) are uniform and independent."""
+    rng = np.random.default_rng(21)
+    xs = [int(x) for x in rng.integers(0, 2 ** 32, 4000, dtype=np.uint64)]
+    for delta in (orc.lowbias32(7) - orc.lowbias32(3), orc.lowbias32(11) - orc.lowbias32(5),
+                  orc.lowbias32(2) - orc.lowbias32(9), 1):
+        delta &= 0xFFFFFFFF
+        diff = np.zeros(32)
+        for x in xs:
+            d = orc.lowbias32_tail(x) ^ orc.lowbias32_tail((x + delta) & 0xFFFFFFFF)
+            diff += [(d >> o) & 1 for o in range(32)]
+        p = diff / len(xs)
+        assert np.all(np.abs(p[2:] - 0.5) < 0.06), (hex(delta), np.abs(p[2:] - 0.5).max())
+    from scipy import stats as st
+    hs = [orc.lowbias32(k) for k in range(20000)]
+    ka = [orc.lowbias32(k * 7 + 3) for k in range(4)]
+    cnt = np.zeros((16, 16))
+    for a in hs:
+        for b in ka:
+            h = orc.lowbias32_tail((a + b) & 0xFFFFFFFF)
+            y = h ^ (h >> 16)
+            cnt[y >> 28, (h >> 10) & 15] += 1
+    chi2, pv, _, _ = st.chi2_contingency(cnt)
+    assert pv > 1e-3
+    assert st.chisquare(cnt.sum(1)).pvalue > 1e-3 and st.chisquare(cnt.sum(0)).pvalue > 1e-3
