@@ -229,6 +229,7 @@ static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, c
   k.height = gb->height;
   k.pitch = gb->pitch;
   k.out_pitch = out_pitch;
+  k.zero = 0u;
   k.sc = *sc;
   return k;
 }

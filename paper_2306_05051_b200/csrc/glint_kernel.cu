@@ -131,6 +131,11 @@ __device__ __forceinline__ float smith_lambda(int kind, float ax2, float ay2, fl
   return __fdividef(__fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f), a * __fmaf_rn(2.181f, a, 3.535f));
 }
 
+// shared tables at namespace scope: fixed shared-window offsets, so the
+// quantile lookup in the draw loop is a single LDS with an immediate base
+__shared__ float g_sZ[GLINT_ZQ];
+__shared__ float2 g_sCS[GLINT_NANG];
+
 // ---------------------------------------------------------------------------
 // Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
 // pixel's output float4, `rec` its first debug record (DEBUG only).
@@ -139,7 +144,7 @@ template <bool DEBUG>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
-                                            uint32_t seed_h, float inv_beta) {
+                                            uint32_t seed_h, float inv_beta, uint32_t zero) {
   const int L = sc.n_lights;
   uint32_t flags = 0;
   const uint32_t meta = __float_as_uint(uvm.w);
@@ -220,9 +225,9 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const uint32_t lin1 = base + (lower ? 0x8da6b343U : 0xd8163841U);
     const uint32_t lin2 = base + (0x8da6b343U + 0xd8163841U);
     const uint32_t h0 = lowbias32(base), h1 = lowbias32(lin1), h2 = lowbias32(lin2);
-    hsC[i * 3 + 0] = opaque(h0 * 0x7feb352dU);
-    hsC[i * 3 + 1] = opaque(h1 * 0x7feb352dU);
-    hsC[i * 3 + 2] = opaque(h2 * 0x7feb352dU);
+    hsC[i * 3 + 0] = (h0 * 0x7feb352dU) ^ zero;
+    hsC[i * 3 + 1] = (h1 * 0x7feb352dU) ^ zero;
+    hsC[i * 3 + 2] = (h2 * 0x7feb352dU) ^ zero;
     if (DEBUG) {
       dlx[i * 3 + 0] = ix; dly[i * 3 + 0] = iy;
       dlx[i * 3 + 1] = lower ? ix + 1u : ix; dly[i * 3 + 1] = lower ? iy : iy + 1u;
@@ -306,7 +311,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
-      kaC[jn] = opaque(lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU);
+      kaC[jn] = (lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU) ^ zero;
     }
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
@@ -370,10 +375,10 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 // ---------------------------------------------------------------------------
 template <bool DEBUG, bool TMA>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
+  float* sZ = g_sZ;
+  float2* sCS = g_sCS;
   extern __shared__ __align__(128) unsigned char smem[];
-  float* sZ = reinterpret_cast<float*>(smem);
-  float2* sCS = reinterpret_cast<float2*>(smem + kSmemZ);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSmemZ + kSmemCS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   float4* tiles = reinterpret_cast<float4*>(smem + kSmemTables);
   const int tid = threadIdx.x;
   for (int i = tid; i < GLINT_ZQ; i += kBlock) sZ[i] = prm.ztab[i];
@@ -434,7 +439,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       oi = (int64_t)y * prm.out_pitch + x;
     }
     shade_pixel<DEBUG>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm, pos,
-                       mat, seed_h, inv_beta);
+                       mat, seed_h, inv_beta, prm.zero);
   }
 }
 

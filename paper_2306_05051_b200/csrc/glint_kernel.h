@@ -17,8 +17,8 @@ constexpr int kBlock = GLINT_BLOCK;
 constexpr int kMinBlocks = GLINT_MIN_BLOCKS;   // resident blocks per SM the register budget targets
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
-constexpr size_t kSmemTables = kSmemZ + kSmemCS + 128;          // + 2 mbarriers per warp (8 warps)
-constexpr size_t kSmemTma = kSmemTables + 2 * 5 * kBlock * 16;  // + per warp 2 x 5 planes x 32 float4
+constexpr size_t kSmemTables = 128;                            // dynamic part: 2 mbarriers (padded)
+constexpr size_t kSmemTma = kSmemTables + 2 * 5 * kBlock * 16;  // + 2 x 5 planes x kBlock float4
 
 struct KParams {
   const float4* duv;
@@ -32,6 +32,8 @@ struct KParams {
   const float2* cstab;  // GLINT_NANG (cos, sin) pairs (device)
   int32_t width, height;
   int64_t pitch, out_pitch;
+  uint32_t zero;        // always 0; XOR-ing pre-multiplied seeds with it stops ptxas
+                        // from re-factoring hs*C1 + ka*C1 into (hs + ka)*C1 per draw
   glint_scene sc;
 };
 
