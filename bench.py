@@ -284,9 +284,11 @@ def run_ours(args):
         "hbm_frac": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9 / float(peaks.get("hbm_gbs", 6458.7)),
         "mean_launch_ms": mean_launch_s * 1e3,
     }
-    if prof and prof.get("sass_thread_inst_per_eval"):
-        roofline["sass_thread_inst_per_eval"] = prof["sass_thread_inst_per_eval"]
-        roofline["issue_frac_sass"] = evals_per_launch * prof["sass_thread_inst_per_eval"] / mean_launch_s / issue_peak
+    if prof and prof.get("sass_thread_inst_per_pixel"):
+        # issue utilisation from the measured SASS count of the last ncu capture
+        roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
+        roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
+        roofline["traffic_source"] = f"profiles/ncu_summary.json ({prof.get('source')})"
     cs = clk.summary()
     if cs.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (sms * LANES_PER_SM * cs["sm_mhz"] * 1e6)
@@ -317,11 +319,14 @@ def run_ours(args):
     # ---- CPU baseline (oracle on host cores), rank 0 at N = 1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        stride = 32 if args.config == "C2" else 256
+        # bounded sample: every 2nd row of the C2 step (~10^7 evals, ~20-30 s of
+        # CPU work on 16 cores; ~2 s wall) / every 32nd row of C4
+        stride = 2 if args.config == "C2" else 32
         subs = oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride)
         ev, t = time_oracle(subs)
         cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-               "sample": f"every {stride}th row of each of the {len(frames)} frames ({ev} evals, {t:.1f} s)"}
+               "sample": f"every {stride}th row of each of the {len(frames)} frames ({ev} evals, {t:.1f} s wall, "
+                         f"{t * host_cores():.0f} core-s)"}
 
     if rank == 0:
         line = {
