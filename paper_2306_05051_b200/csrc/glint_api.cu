@@ -235,7 +235,7 @@ static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, c
 }
 
 static int grid_for(const glint_ctx* c, int64_t n_pix) {
-  int64_t need = (n_pix + glint::kBlock - 1) / glint::kBlock;
+  int64_t need = (n_pix + glint::kTile - 1) / glint::kTile;
   int64_t cap = (int64_t)c->sm_count * c->blocks_per_sm;
   return (int)(need < cap ? need : cap);
 }
