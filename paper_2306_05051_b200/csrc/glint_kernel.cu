@@ -317,99 +317,32 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
     const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
-    float C;
-    if (DEBUG) {
-      // dense reference loop: every draw's hash and count recorded
-      float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // A_j = sum_ik beta_ik c_ikj
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const Gate gt = gate_params(n[i], p, L2);
-        const uint32_t G = (gt.T << 9) - 1u;
-        const float capk = gt.T ? gt.cap : 0.0f;
-        rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap;
+    for (int i = 0; i < 4; ++i) {
+      const Gate gt = gate_params(n[i], p, L2);
+      // gate (y >> 9) < T  <=>  y <= T*512 - 1; T = 0 wraps to "always" but its
+      // cap is forced to 0 so the count is 0 (same result, one compare)
+      const uint32_t G = (gt.T << 9) - 1u;
+      const float capk = gt.T ? gt.cap : 0.0f;
+      if (DEBUG) { rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap; }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < 3; ++k) {
+        const float bk = beta[i * 3 + k];
 #pragma unroll
-          for (int jn = 0; jn < 4; ++jn) {
-            uint32_t y = hsC[i * 3 + k] + kaC[jn];
-            y ^= y >> 15;
-            y *= 0x846ca68bU;
-            const uint32_t h = y ^ (y >> 16);
-            const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
-            const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
-            const bool pass = y <= G;
-            if (pass) A[jn] = __fmaf_rn(beta[i * 3 + k], c, A[jn]);
-            rc->hash[i * 12 + k * 4 + jn] = h;
-            rc->count[i * 12 + k * 4 + jn] = pass ? c : 0.0f;
-          }
-        }
-      }
-      C = __fmaf_rn(vj[3], A[3], __fmaf_rn(vj[2], A[2], __fmaf_rn(vj[1], A[1], vj[0] * A[0])));
-    } else {
-      // Production: glints are sparse (on C2 a warp has ~1 passing draw per
-      // pixel-light out of 48), so per grid the 12 gates are evaluated
-      // branch-free into a bit mask and only the passing draws compute their
-      // quantile, clamp and floor, in a warp-uniform loop. Counts are the
-      // same as the dense loop's; only the fp32 summation order of C differs.
-      C = 0.0f;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const Gate gt = gate_params(n[i], p, L2);
-        const uint32_t G = (gt.T << 9) - 1u;
-        const float capk = gt.T ? gt.cap : 0.0f;
-        uint32_t mk = 0;   // bit k*4 + jn: draw (k, jn) passes its gate
-        uint32_t yv[12];   // the 12 draws' hashes (before the final xor-shift)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-#pragma unroll
-          for (int jn = 0; jn < 4; ++jn) {
-            uint32_t y = hsC[i * 3 + k] + kaC[jn];
-            y ^= y >> 15;
-            y *= 0x846ca68bU;
-            yv[k * 4 + jn] = y;
-            if (y <= G) mk += 1u << (k * 4 + jn);
-          }
-        }
-        const uint32_t hs0 = hsC[i * 3 + 0], hs1 = hsC[i * 3 + 1], hs2 = hsC[i * 3 + 2];
-        const float b0 = beta[i * 3 + 0], b1 = beta[i * 3 + 1], b2 = beta[i * 3 + 2];
-        const uint32_t wmax = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(mk));
-        if (wmax > kDenseThreshold) {
-          // dense grid (e.g. far, large footprints): all 12 bodies, branch-free
-          float A4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-          for (int k = 0; k < 3; ++k) {
-#pragma unroll
-            for (int jn = 0; jn < 4; ++jn) {
-              const uint32_t y = yv[k * 4 + jn];
-              const uint32_t h = y ^ (y >> 16);
-              const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
-              const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
-              if (mk & (1u << (k * 4 + jn))) A4[jn] = __fmaf_rn(beta[i * 3 + k], c, A4[jn]);
-            }
-          }
-          C = __fmaf_rn(vj[3], A4[3], __fmaf_rn(vj[2], A4[2], __fmaf_rn(vj[1], A4[1], __fmaf_rn(vj[0], A4[0], C))));
-          mk = 0u;
-        }
-        while (__any_sync(0xffffffffu, mk != 0u)) {
-          if (mk != 0u) {
-            const int bit = __ffs(mk) - 1;
-            mk &= mk - 1u;
-            const int k = bit >> 2, jn = bit & 3;
-            const uint32_t hs = k == 0 ? hs0 : (k == 1 ? hs1 : hs2);
-            const float bk = k == 0 ? b0 : (k == 1 ? b1 : b2);
-            const uint32_t ka = jn < 2 ? (jn == 0 ? kaC[0] : kaC[1]) : (jn == 2 ? kaC[2] : kaC[3]);
-            const float vv = jn < 2 ? (jn == 0 ? vj[0] : vj[1]) : (jn == 2 ? vj[2] : vj[3]);
-            uint32_t y = hs + ka;
-            y ^= y >> 15;
-            y *= 0x846ca68bU;
-            const uint32_t h = y ^ (y >> 16);
-            const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + (h & 0x3FFCu));
-            const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
-            C = __fmaf_rn(bk * vv, c, C);
-          }
+        for (int jn = 0; jn < 4; ++jn) {
+          uint32_t y = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
+          y ^= y >> 15;
+          y *= 0x846ca68bU;                              // y: gate bits 9..31
+          const uint32_t s16 = y >> 16;                  // h = y ^ (y >> 16): quantile bits 2..13
+          const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
+          const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
+          if (y <= G) A[jn] = __fmaf_rn(bk, c, A[jn]);
+          if (DEBUG) { rc->hash[i * 12 + k * 4 + jn] = y ^ s16; rc->count[i * 12 + k * 4 + jn] = (y <= G) ? c : 0.0f; }
         }
       }
     }
+    const float C = __fmaf_rn(vj[3], A[3], __fmaf_rn(vj[2], A[2], __fmaf_rn(vj[1], A[1], vj[0] * A[0])));
     if (DEBUG) { rc->C = C; rc->Dp = C * dp_scale; (void)dhs; }
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
     if (C > 0.0f) {
@@ -433,12 +366,11 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 }
 
 // ---------------------------------------------------------------------------
-// The kernel: persistent blocks over tiles of kTile pixels. TMA (contiguous
-// G-buffer, pitch == width): a kStages-deep ring of tile buffers filled by the
-// bulk-copy engine (cp.async.bulk, one transaction-count mbarrier per stage).
-// There is no block-wide barrier: each warp waits only for its data, and the
-// last warp to release a stage (shared-memory counter) refills it with the
-// tile kStages ahead, so warps may drift up to kStages-1 tiles apart.
+// The kernel: persistent blocks over 256-pixel tiles. TMA (contiguous
+// G-buffer, pitch == width): one thread issues the 5 bulk copies (5 x 4 KB)
+// of the block's next tile into the second buffer while the block shades the
+// current one (mbarrier-tracked, double-buffered); the block stays in step,
+// which keeps its warps in the same code (instruction-cache friendly).
 // Otherwise the planes are read directly.
 // ---------------------------------------------------------------------------
 template <bool DEBUG, bool TMA>
@@ -446,14 +378,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   float* sZ = g_sZ;
   float2* sCS = g_sCS;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint32_t* rel = reinterpret_cast<uint32_t*>(smem + 8 * kStages);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   float4* tiles = reinterpret_cast<float4*>(smem + kSmemTables);
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   for (int i = tid; i < GLINT_ZQ; i += kBlock) sZ[i] = prm.ztab[i];
   for (int i = tid; i < GLINT_NANG; i += kBlock) sCS[i] = prm.cstab[i];
   if (TMA && tid == 0) {
-    for (int st = 0; st < kStages; ++st) { mbar_init(&full[st], 1); rel[st] = 0u; }
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -464,28 +396,29 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   const float inv_beta = 1.0f / sc.beta;
   const uint32_t seed_h = lowbias32(sc.seed);
   const bool flat_out = prm.out_pitch == prm.width;
-  const int64_t gstride = gridDim.x;
 
-  auto issue = [&](int64_t t, int st) {   // one thread: 5 bulk copies of tile t into stage st
+  auto issue = [&](int64_t t, int b) {   // one thread: 5 bulk copies of tile t into buffer b
     const int64_t base = t * kTile;
     const int64_t cnt = (n_pix - base) < kTile ? (n_pix - base) : kTile;
     const uint32_t bytes = (uint32_t)cnt * 16u;
     fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&full[st], 5u * bytes);
-    bulk_g2s(tiles + (st * 5 + 0) * kTile, prm.duv + base, bytes, &full[st]);
-    bulk_g2s(tiles + (st * 5 + 1) * kTile, prm.uvm + base, bytes, &full[st]);
-    bulk_g2s(tiles + (st * 5 + 2) * kTile, prm.nrm + base, bytes, &full[st]);
-    bulk_g2s(tiles + (st * 5 + 3) * kTile, prm.pos + base, bytes, &full[st]);
-    bulk_g2s(tiles + (st * 5 + 4) * kTile, prm.mat + base, bytes, &full[st]);
+    mbar_arrive_expect_tx(&bars[b], 5u * bytes);
+    bulk_g2s(tiles + (b * 5 + 0) * kTile, prm.duv + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 1) * kTile, prm.uvm + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 2) * kTile, prm.nrm + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 3) * kTile, prm.pos + base, bytes, &bars[b]);
+    bulk_g2s(tiles + (b * 5 + 4) * kTile, prm.mat + base, bytes, &bars[b]);
   };
 
   int64_t t = blockIdx.x;
-  if (TMA && tid == 0)
-    for (int st = 0; st < kStages; ++st)
-      if (t + st * gstride < n_tiles) issue(t + st * gstride, st);
-  for (int it = 0; t < n_tiles; t += gstride, ++it) {
-    const int st = it % kStages;
-    if (TMA) mbar_wait(&full[st], (uint32_t)(it / kStages) & 1u);
+  if (TMA && tid == 0 && t < n_tiles) issue(t, 0);
+  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    if (TMA) {
+      __syncthreads();   // the whole block is done reading buffer b^1 (iteration it-1)
+      if (tid == 0 && t + gridDim.x < n_tiles) issue(t + gridDim.x, b ^ 1);
+      mbar_wait(&bars[b], (uint32_t)(it >> 1) & 1u);
+    }
 #pragma unroll 1
     for (int q = 0; q < kPPT; ++q) {
       const int slot = q * kBlock + tid;
@@ -494,7 +427,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       float4 duv, uvm, nrm, pos, mat;
       int64_t oi = idx;
       if (TMA) {
-        const float4* tb = tiles + st * 5 * kTile + slot;
+        const float4* tb = tiles + b * 5 * kTile + slot;
         duv = tb[0]; uvm = tb[kTile]; nrm = tb[2 * kTile]; pos = tb[3 * kTile]; mat = tb[4 * kTile];
         if (!flat_out) {
           const uint32_t y = (uint32_t)idx / (uint32_t)prm.width;
@@ -507,20 +440,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
         duv = __ldcs(prm.duv + gi); uvm = __ldcs(prm.uvm + gi); nrm = __ldcs(prm.nrm + gi);
         pos = __ldcs(prm.pos + gi); mat = __ldcs(prm.mat + gi);
         oi = (int64_t)y * prm.out_pitch + x;
-      }
-      if (TMA && q == kPPT - 1) {
-        // this warp has read its last pixel of the stage: release it; the last
-        // of the block's warps refills the stage with the tile kStages ahead
-        __syncwarp();
-        if (lane == 0) {
-          __threadfence_block();
-          const uint32_t old = atomicAdd(&rel[st], 1u);
-          if (old == (uint32_t)(kBlock / 32 - 1)) {
-            rel[st] = 0u;
-            const int64_t nt = t + (int64_t)kStages * gstride;
-            if (nt < n_tiles) issue(nt, st);
-          }
-        }
       }
       shade_pixel<DEBUG>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm,
                          pos, mat, seed_h, inv_beta, prm.zero);

@@ -16,24 +16,14 @@ constexpr int kBlock = GLINT_BLOCK;
 #endif
 constexpr int kMinBlocks = GLINT_MIN_BLOCKS;   // resident blocks per SM the register budget targets
 #ifndef GLINT_PPT
-#define GLINT_PPT 1
+#define GLINT_PPT 2
 #endif
-#ifndef GLINT_STAGES
-#define GLINT_STAGES 3
-#endif
-constexpr int kStages = GLINT_STAGES;           // TMA ring depth (tiles in flight per block)
-#ifndef GLINT_DENSE_T
-#define GLINT_DENSE_T 1
-#endif
-// a grid whose warp has more than this many passing draws (of 12) takes the
-// dense branch-free body instead of the sparse per-pass loop
-constexpr uint32_t kDenseThreshold = GLINT_DENSE_T;
 constexpr int kPPT = GLINT_PPT;                 // pixels per thread per TMA tile
 constexpr int kTile = kBlock * kPPT;            // pixels per tile
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
-constexpr size_t kSmemTables = 128;            // dynamic part: kStages mbarriers + release counters (padded)
-constexpr size_t kSmemTma = kSmemTables + (size_t)kStages * 5 * kTile * 16;  // + kStages x 5 planes x kTile float4
+constexpr size_t kSmemTables = 128;                            // dynamic part: 2 mbarriers (padded)
+constexpr size_t kSmemTma = kSmemTables + 2 * 5 * (size_t)kTile * 16;  // + 2 x 5 planes x kTile float4
 
 struct KParams {
   const float4* duv;

@@ -54,12 +54,18 @@ def compare_radiance(out, rgb_o, fl_o, where=""):
 
 
 def run_both(ctx, gb, scene, debug=True):
+    """Oracle vs GPU. With debug=True the DEBUG instantiation writes records
+    (dense reference loop); the production instantiation (sparse gates, warp
+    votes) runs too and must give the same flags and radiance."""
     import oracle
     import paper_2306_05051_b200 as pkg
     gd = gb.to("cuda")
     res = pkg.glint_eval(ctx, gd, scene, debug=debug)
+    prod = pkg.glint_eval(ctx, gd, scene) if debug else None
     torch.cuda.synchronize()
     rgb_o, fl_o, rec_o = oracle.eval(gb, scene, debug=debug)
+    if prod is not None:
+        compare_radiance(prod, rgb_o, fl_o, "production kernel")
     return res, (rgb_o, fl_o, rec_o)
 
 
@@ -157,6 +163,24 @@ def test_full_size_c2_sampled(ctx):
         sub = fr.gbuf.take(idx).to("cpu")
         rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
         compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, f"full{elev}")
+
+
+@pytest.mark.timeout(300)
+def test_full_size_c4_sampled(ctx):
+    """A full 3840x2160 C4 frame (32 spheres, 16 lights) in the bench's launch
+    configuration (production kernel: sparse gates and warp votes over lanes
+    with mixed light visibility); sampled pixels recomputed by the oracle."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c4(2, device="cuda")
+    out = pkg.glint_eval(ctx, fr.gbuf, fr.scene).reshape(-1, 4)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(1)
+    idx = torch.randint(0, 3840 * 2160, (1500,), generator=g)
+    sub = fr.gbuf.take(idx).to("cpu")
+    rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+    compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "C4 full")
 
 
 def test_tables_on_device(ctx, orc):
