@@ -136,7 +136,9 @@ struct Gate {
 };
 __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   // L2 = log2(1 - p) for p in (0,1), precomputed once per (pixel, light)
-  // branch-free: all candidates computed, selected
+  // branch-free. For n <= 0 or p <= 0 only T needs forcing (to 0): the
+  // sigma / m1 / cap of such a grid are never used (its count is 0), and
+  // the DEBUG record reports the contract's values (0, 1, 1) explicitly.
   Gate g;
   const bool none = !(n > 0.0f) || !(p > 0.0f);
   const float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
@@ -144,11 +146,10 @@ __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   const float nm1 = n - 1.0f;
   const float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
   const float var = mu * (1.0f - p);
-  const float sg = var > 0.0f ? var * rsqrt_c(var) : 0.0f;   // sqrt via the contract rsqrt
   g.T = none ? 0u : T;
-  g.sigma = none ? 0.0f : sg;
-  g.m1 = none ? 1.0f : 1.0f + mu;
-  g.cap = none ? 1.0f : ceilf(n);
+  g.sigma = var > 0.0f ? var * rsqrt_c(var) : 0.0f;   // sqrt via the contract rsqrt
+  g.m1 = 1.0f + mu;
+  g.cap = ceilf(n);
   return g;
 }
 

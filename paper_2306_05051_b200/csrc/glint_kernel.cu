@@ -208,8 +208,10 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const float2 cs = sCS[sl[i].jo << (8 - sl[i].lr)];
     const float xr = __fmaf_rn(cs.x, u, cs.y * v);
     const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
-    const float gx = xr * pow2half(-(sl[i].ls + sl[i].lr));
-    const float gy = yr * pow2half(sl[i].lr - sl[i].ls);
+    // 2^((lr-ls)/2) = 2^(-(ls+lr)/2) * 2^lr exactly (power-of-two scaling)
+    const float sxs = pow2half(-(sl[i].ls + sl[i].lr));
+    const float gx = xr * sxs;
+    const float gy = yr * (sxs * pow2i(sl[i].lr));
     const float xs = gx + 0.5f * gy;
     const float fxs = floorf(xs), fys = floorf(gy);
     const float fx = xs - fxs, fy = gy - fys;
@@ -251,12 +253,11 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
   const float iax = 1.0f / ax, iay = 1.0f / ay;
   // radiance-path constants (tolerance path: fast intrinsics allowed)
+  // radiance-path constants, computed on first use (most pixels receive no
+  // glint from any light: C = 0)
   const float ax2 = ax * ax, ay2 = ay * ay;
-  const float lam_i = smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wix, wiy, wiz, tx, ty, tz),
-                                   dot3(wix, wiy, wiz, bx, by, bz), ni);
-  // D_P / (4 n.wi) = C D(n) / (R N P 4 n.wi), D(n) = 1/(pi ax ay)  (Eq. 2-4, R-20)
-  const float dp_scale = __fdividef(1.0f, 3.14159265358979f * ax * ay * R * N * P);
-  const float rad_scale = __fdividef(dp_scale, 4.0f * ni);
+  float lam_i = 0.0f, dp_scale = 0.0f, rad_scale = 0.0f;
+  bool have_rad = false;
   float3 rgb = make_float3(0.0f, 0.0f, 0.0f);
 
   for (int l = 0; l < L; ++l) {
@@ -325,7 +326,13 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       // cap is forced to 0 so the count is 0 (same result, one compare)
       const uint32_t G = (gt.T << 9) - 1u;
       const float capk = gt.T ? gt.cap : 0.0f;
-      if (DEBUG) { rc->T[i] = gt.T; rc->sigma[i] = gt.sigma; rc->m1[i] = gt.m1; rc->cap[i] = gt.cap; }
+      if (DEBUG) {
+        const bool none = !(n[i] > 0.0f) || !(p > 0.0f);
+        rc->T[i] = gt.T;
+        rc->sigma[i] = none ? 0.0f : gt.sigma;
+        rc->m1[i] = none ? 1.0f : gt.m1;
+        rc->cap[i] = none ? 1.0f : gt.cap;
+      }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float bk = beta[i * 3 + k];
@@ -343,6 +350,13 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       }
     }
     const float C = __fmaf_rn(vj[3], A[3], __fmaf_rn(vj[2], A[2], __fmaf_rn(vj[1], A[1], vj[0] * A[0])));
+    if (DEBUG || (C > 0.0f && !have_rad)) {
+      lam_i = smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wix, wiy, wiz, tx, ty, tz), dot3(wix, wiy, wiz, bx, by, bz), ni);
+      // D_P / (4 n.wi) = C D(n) / (R N P 4 n.wi), D(n) = 1/(pi ax ay)  (Eq. 2-4, R-20)
+      dp_scale = __fdividef(1.0f, 3.14159265358979f * ax * ay * R * N * P);
+      rad_scale = __fdividef(dp_scale, 4.0f * ni);
+      have_rad = true;
+    }
     if (DEBUG) { rc->C = C; rc->Dp = C * dp_scale; (void)dhs; }
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
     if (C > 0.0f) {
