@@ -172,6 +172,8 @@ def run_reference(args):
     if rank != 0:
         return 0
     frames, desc = make_frames(args.config, "cpu", seed=1)
+    for fr in frames:
+        fr.scene.draws = args.draws
     stride = 64 if args.config == "C2" else 256
     subs = oracle_sample(frames, stride)
     cores = host_cores()
@@ -219,6 +221,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     ctx = pkg.Context(local)
     frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank)
+    for fr in frames:
+        fr.scene.draws = args.draws
+    if args.draws != 48:
+        desc += f"; ABLATION: {args.draws} draws per pixel-light (P:L749/L758)"
     tot_px, valid_px, evals = count_evals(frames)
     outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
     stream = torch.cuda.current_stream(dev)
@@ -354,6 +360,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--draws", type=int, default=48, choices=[48, 64, 160],
+                    help="draws per pixel-light: 48 = the method; 64 / 160 = its section-6 ablations")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

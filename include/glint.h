@@ -42,7 +42,8 @@ extern "C" {
 
 /* return codes */
 #define GLINT_OK 0
-#define GLINT_EINVAL -1   /* null pointer, size <= 0, bad enum, K not in [1,8], beta <= 0, n_lights not in [0,16] */
+#define GLINT_EINVAL -1   /* null pointer, size < 0, bad enum, K not in [1,8], beta <= 0, n_lights not in [0,16],
+                             eval_mode not in [0,2] or debug records requested with eval_mode != 0 */
 #define GLINT_EALIGN -2   /* a plane / output pointer not 16-byte aligned, pitch < width */
 #define GLINT_EDEVICE -3  /* no CUDA device, device is not sm_100, or ctx/device mismatch */
 #define GLINT_ELIMIT -4   /* width*height or pitch*height >= 2^31 pixels */
@@ -82,7 +83,11 @@ typedef struct {
   int32_t view_kind;        /* 0 = pinhole camera at view[], 1 = directional view[] */
   float view[3];
   int32_t n_lights;         /* 0 .. GLINT_MAX_LIGHTS */
-  int32_t reserved[4];
+  int32_t eval_mode;        /* draws per (pixel, light): 0 = 48, the paper's method (4 tetrahedron
+                               grids x 3 simplex texels x 4 angular nodes); ablations of
+                               its section 6: 1 = 64 (4 grids x 4 bilinear texels
+                               x 4), 2 = 160 (10 prism grids x 4 x 4). Debug records: mode 0 only */
+  int32_t reserved[3];
   glint_light lights[GLINT_MAX_LIGHTS];
 } glint_scene;
 

@@ -52,7 +52,7 @@ class _Scene(C.Structure):
     _fields_ = [("seed", C.c_uint32), ("ndf_kind", C.c_int32), ("max_ratio_level", C.c_int32),
                 ("beta", C.c_float), ("f0", C.c_float * 3), ("view_kind", C.c_int32),
                 ("view", C.c_float * 3), ("n_lights", C.c_int32), ("sampler", C.c_int32),
-                ("pad_", C.c_int32 * 3), ("lights", _Light * MAX_LIGHTS)]
+                ("eval_mode", C.c_int32), ("pad_", C.c_int32 * 2), ("lights", _Light * MAX_LIGHTS)]
 
 
 REC_DTYPE = np.dtype([
@@ -93,6 +93,9 @@ def lib():
             i4p = C.POINTER(C.c_int32)
             L.orc_lattice.argtypes = [C.c_float, C.c_float, C.c_float, C.c_int32, i4p, i4p, i4p, fp,
                                       C.POINTER(C.c_uint32)]
+            i4p10 = C.POINTER(C.c_int32)
+            L.orc_lattice10.argtypes = [C.c_float, C.c_float, C.c_float, C.c_int32, i4p10, i4p10, i4p10, fp,
+                                        C.POINTER(C.c_uint32)]
             L.orc_grid_uv.argtypes = [C.c_float, C.c_float, C.c_int32, C.c_int32, C.c_int32, fp, fp]
             L.orc_grid_uv.restype = None
             i8p = C.POINTER(C.c_int64)
@@ -142,6 +145,7 @@ def scene_struct(scene, sampler: str = "gated") -> _Scene:
         raise ValueError("too many lights")
     s.n_lights = len(scene.lights)
     s.sampler = {"gated": 0, "exact": 1}[sampler]
+    s.eval_mode = {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
     for i, lt in enumerate(scene.lights):
         s.lights[i].kind = 0 if lt.kind == "point" else 1
         s.lights[i].pos_or_dir[:] = [float(x) for x in lt.pos_or_dir]
@@ -233,6 +237,14 @@ def lattice(P: float, r: float, psi: float, K: int = 8):
     w = (C.c_float * 4)()
     fl = C.c_uint32(0)
     lib().orc_lattice(P, r, psi, K, ls, lr, jo, w, C.byref(fl))
+    return list(ls), list(lr), list(jo), list(w), fl.value
+
+
+def lattice10(P: float, r: float, psi: float, K: int = 8):
+    ls, lr, jo = (C.c_int32 * 10)(), (C.c_int32 * 10)(), (C.c_int32 * 10)()
+    w = (C.c_float * 10)()
+    fl = C.c_uint32(0)
+    lib().orc_lattice10(P, r, psi, K, ls, lr, jo, w, C.byref(fl))
     return list(ls), list(lr), list(jo), list(w), fl.value
 
 

@@ -311,6 +311,60 @@ int orc_lattice(float P, float r, float psi, int32_t K, int32_t ls[4], int32_t l
   return 0;
 }
 
+/* The naive 10-grid distribution the paper starts from before its tetrahedral
+ * split ("2 x 5 anisotropic grids with linear blending"; "trilinear
+ * weights"), reading R-29: linear in ts between the two LODs, linear
+ * in tr between the two ratio rings, linear in a between the inner ring's two
+ * orientations and piecewise linear (hats at a = 0, 1/2, 1) over the outer
+ * ring's three. Slots: LOD es then es+1, each A00 A01 A10 A11 A12; coincident
+ * ring-0 vertices merged as in R-13. Used only by the 160-draw ablation. */
+int orc_lattice10(float P, float r, float psi, int32_t K, int32_t ls[10], int32_t lr[10],
+                  int32_t jo[10], float w[10], uint32_t* flags) {
+  uint32_t pb = f2u(P);
+  int32_t es = (int32_t)((pb >> 23) & 255u) - 127;
+  float ts = u2f((pb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+  int32_t er;
+  float tr;
+  if (!(r >= 1.0f)) r = 1.0f;
+  if (r >= pow2i(K)) {
+    if (r > pow2i(K)) *flags |= ORC_FLAG_RATIO_CLAMPED;
+    er = K - 1;
+    tr = 1.0f;
+  } else {
+    uint32_t rb = f2u(r);
+    er = (int32_t)((rb >> 23) & 255u) - 127;
+    tr = u2f((rb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+  }
+  float A = psi * pow2i(er);
+  float jf = floorf(A);
+  float a = A - jf;
+  int32_t j = (int32_t)jf;
+  int32_t nI = 1 << er, nO = 2 << er;
+  int32_t vlr[5] = {er, er, er + 1, er + 1, er + 1};
+  int32_t vjo[5] = {j, (j + 1) & (nI - 1), 2 * j, 2 * j + 1, (2 * j + 2) & (nO - 1)};
+  float a2 = a + a;
+  float omt = 1.0f - tr;
+  float pw[5];
+  pw[0] = omt * (1.0f - a);
+  pw[1] = omt * a;
+  pw[2] = tr * (a2 <= 1.0f ? 1.0f - a2 : 0.0f);
+  pw[3] = tr * (a2 <= 1.0f ? a2 : 2.0f - a2);
+  pw[4] = tr * (a2 <= 1.0f ? 0.0f : a2 - 1.0f);
+  for (int p = 0; p < 5; ++p)
+    for (int q = p + 1; q < 5; ++q)
+      if (vlr[p] == vlr[q] && vjo[p] == vjo[q]) { pw[p] = pw[p] + pw[q]; pw[q] = 0.0f; }
+  for (int lv = 0; lv < 2; ++lv) {
+    float sw = lv ? ts : 1.0f - ts;
+    for (int p = 0; p < 5; ++p) {
+      ls[lv * 5 + p] = es + lv;
+      lr[lv * 5 + p] = vlr[p];
+      jo[lv * 5 + p] = vjo[p];
+      w[lv * 5 + p] = sw * pw[p];
+    }
+  }
+  return 0;
+}
+
 /* ---------------------------------------------------------------------- */
 /* S3  Anisotropic grid transform (Eq. 12, reading R-14):
  * rotate by phi_j = m pi / 256 (m = jo 2^(8-lr)), then area-preserving stretch:
@@ -349,6 +403,18 @@ void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]) 
     lx[1] = ix;     ly[1] = iy + 1; beta[1] = fy - fx;
     lx[2] = ix + 1; ly[2] = iy + 1; beta[2] = fx;
   }
+}
+
+/* Square spatial grid with bilinear weights (the 4-texel spatial blending the
+ * simplex grid replaces); used by the 64- and 160-draw ablations. */
+void orc_bilinear(float x, float y, int64_t lx[4], int64_t ly[4], float beta[4]) {
+  float fxs = floorf(x), fys = floorf(y);
+  float fx = x - fxs, fy = y - fys;
+  int64_t ix = (int64_t)fxs, iy = (int64_t)fys;
+  lx[0] = ix;     ly[0] = iy;     beta[0] = (1.0f - fx) * (1.0f - fy);
+  lx[1] = ix + 1; ly[1] = iy;     beta[1] = fx * (1.0f - fy);
+  lx[2] = ix;     ly[2] = iy + 1; beta[2] = (1.0f - fx) * fy;
+  lx[3] = ix + 1; ly[3] = iy + 1; beta[3] = fx * fy;
 }
 
 /* ---------------------------------------------------------------------- */
@@ -497,35 +563,47 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
   float P, r, psi;
   if (!orc_footprint(duv, &P, &r, &psi)) { *flags_out = ORC_FLAG_DEGENERATE; goto fill_flags; }
 
-  /* S2 lattice: 4 grids + distribution weights; n_i = w_i N 2^ls_i (R-14:
-   * "N_i proportional to its area") */
-  int32_t ls[4], lr[4], jo[4];
-  float w[4], n[4];
-  orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
+  /* S2 lattice: 4 grids (tetrahedron of the prism) + distribution
+   * weights; n_i = w_i N 2^ls_i (R-14: "N_i proportional to its area",
+   * P:L633). Ablation mode 2 (160 draws) uses all 10 prism vertices (R-29). */
+  const int mode = sc->eval_mode;
+  const int NG = mode == 2 ? 10 : 4;          /* grids */
+  const int NS = mode == 0 ? 3 : 4;           /* spatial texels per grid */
+  int32_t ls[10], lr[10], jo[10];
+  float w[10], n[10];
+  if (mode == 2) orc_lattice10(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
+  else orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
   float N = mat[2], R = mat[3], ax = mat[0], ay = mat[1];
-  for (int i = 0; i < 4; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
+  for (int i = 0; i < NG; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
 
-  /* S3 + S4a: per grid, 3 simplex lattice vertices and their spatial seeds */
+  /* S3 + S4a: per grid, 3 simplex lattice vertices -- or, in the
+   * 64/160 ablations, 4 square-lattice texels with bilinear weights -- and
+   * their spatial seeds */
   uint32_t obj = f2u(uvm[2]);
   uint32_t so = orc_lowbias32(obj ^ orc_lowbias32(sc->seed));
-  uint32_t hs[4][3];
-  int64_t lxs[4][3], lys[4][3];
-  double betad[4][3];
-  for (int i = 0; i < 4; ++i) {
-    float x, y, be[3];
+  uint32_t hs[10][4];
+  int64_t lxs[10][4], lys[10][4];
+  double betad[10][4];
+  for (int i = 0; i < NG; ++i) {
+    float x, y, be[4];
     orc_grid_uv(u, v, ls[i], lr[i], jo[i], &x, &y);
-    orc_simplex(x, y, lxs[i], lys[i], be);
-    /* barycentrics recomputed in fp64 from the exact fp32 fractions */
-    {
+    if (mode == 0) {
+      orc_simplex(x, y, lxs[i], lys[i], be);
+      /* barycentrics recomputed in fp64 from the exact fp32 fractions */
       float xs = x + 0.5f * y;
       double fx = (double)(xs - floorf(xs)), fy = (double)(y - floorf(y));
       if (fx >= fy) { betad[i][0] = 1.0 - fx; betad[i][1] = fx - fy; betad[i][2] = fy; }
       else          { betad[i][0] = 1.0 - fy; betad[i][1] = fy - fx; betad[i][2] = fx; }
+    } else {
+      orc_bilinear(x, y, lxs[i], lys[i], be);
+      double fx = (double)(x - floorf(x)), fy = (double)(y - floorf(y));
+      betad[i][0] = (1.0 - fx) * (1.0 - fy); betad[i][1] = fx * (1.0 - fy);
+      betad[i][2] = (1.0 - fx) * fy;         betad[i][3] = fx * fy;
     }
     /* spatial seed of texel (grid key, lattice vertex): one hash of the
      * object/seed word plus a linear code of (key, lx, ly) (reading R-23) */
     uint32_t gk = ((uint32_t)ls[i] & 511u) | ((uint32_t)lr[i] << 9) | ((uint32_t)jo[i] << 13);
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < NS; ++k) {
       uint32_t lin = gk * 0x9e3779b1U + (uint32_t)lxs[i][k] * 0x8da6b343U + (uint32_t)lys[i][k] * 0xd8163841U;
       hs[i][k] = orc_lowbias32(so + lin);
     }
@@ -592,14 +670,15 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     }
     if (rc) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
-    /* S6 + S7 + S8: 4 grids x 3 spatial x 4 angular = 48 draws */
+    /* S6 + S7 + S8: 4 grids x 3 spatial x 4 angular = 48 draws
+     * (ablations: 4 x 4 x 4 = 64; 10 x 4 x 4 = 160) */
     double C = 0.0;
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < NG; ++i) {
       uint32_t T; float sig, m1, cap;
       orc_gate_params(n[i], p, &T, &sig, &m1, &cap);
       if (rc) { rc->T[i] = T; rc->sigma[i] = sig; rc->m1[i] = m1; rc->cap[i] = cap; }
       double Ci = 0.0; /* b_theta_i(w_i N_i, p), interpolated (Eq. 14, R-16) */
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < NS; ++k) {
         double Cik = 0.0;
         for (int jn = 0; jn < 4; ++jn) {
           uint32_t h = orc_lowbias32_tail(hs[i][k] + ka[jn]);
@@ -609,7 +688,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
         }
         Ci += betad[i][k] * Cik;
       }
-      C += Ci; /* distributed law: sum over the 4 grids (Eq. 10/13) */
+      C += Ci; /* distributed law: sum over the grids (Eq. 10/13) */
     }
 
     /* S8: Eq. 3-4, D_P = D(n)/R * b / N(P), N(P) = N P (reading R-20) */
@@ -651,6 +730,8 @@ int orc_eval(const float* duv, const float* uvm, const float* nrm, const float* 
              uint32_t* flags, orc_rec* rec) {
   orc_init();
   if (sc->n_lights < 0 || sc->n_lights > ORC_MAX_LIGHTS) return -1;
+  if (sc->eval_mode < 0 || sc->eval_mode > 2) return -1;
+  if (rec && sc->eval_mode != 0) return -1;   /* debug records describe the 48-draw path */
   for (int64_t i = 0; i < n; ++i)
     eval_pixel(duv + 4 * i, uvm + 4 * i, nrm + 4 * i, pos + 4 * i, mat + 4 * i, sc,
                rgb + 3 * i, flags + i, rec ? rec + i * sc->n_lights : 0);

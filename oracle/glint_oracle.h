@@ -45,7 +45,10 @@ typedef struct {
   float view[3];
   int32_t n_lights;
   int32_t sampler;         /* 0 = gated Gaussian (Eq. 18), 1 = exact Bernoulli sum (tests) */
-  int32_t pad_[3];
+  int32_t eval_mode;       /* draws per pixel-light: 0 = 48 (tetrahedra x simplex x angular),
+                              1 = 64 (tetrahedra x bilinear x angular), 2 = 160 (10 prism
+                              vertices x bilinear x angular) -- P:L749, L758, L928 */
+  int32_t pad_[2];
   orc_light lights[ORC_MAX_LIGHTS];
 } orc_scene;
 
@@ -89,6 +92,9 @@ uint32_t orc_lowbias32_tail(uint32_t x);
 int orc_footprint(const float duv[4], float* P, float* r, float* psi);
 int orc_lattice(float P, float r, float psi, int32_t K, int32_t ls[4], int32_t lr[4],
                 int32_t jo[4], float w[4], uint32_t* flags);
+int orc_lattice10(float P, float r, float psi, int32_t K, int32_t ls[10], int32_t lr[10],
+                  int32_t jo[10], float w[10], uint32_t* flags);
+void orc_bilinear(float x, float y, int64_t lx[4], int64_t ly[4], float beta[4]);
 void orc_grid_uv(float u, float v, int32_t ls, int32_t lr, int32_t jo, float* x, float* y);
 void orc_simplex(float x, float y, int64_t lx[3], int64_t ly[3], float beta[3]);
 void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap);

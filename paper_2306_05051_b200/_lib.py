@@ -42,7 +42,8 @@ class glint_light(C.Structure):
 class glint_scene(C.Structure):
     _fields_ = [("seed", C.c_uint32), ("ndf_kind", C.c_int32), ("max_ratio_level", C.c_int32),
                 ("beta", C.c_float), ("f0", C.c_float * 3), ("view_kind", C.c_int32), ("view", C.c_float * 3),
-                ("n_lights", C.c_int32), ("reserved", C.c_int32 * 4), ("lights", glint_light * MAX_LIGHTS)]
+                ("n_lights", C.c_int32), ("eval_mode", C.c_int32), ("reserved", C.c_int32 * 3),
+                ("lights", glint_light * MAX_LIGHTS)]
 
 
 class glint_gbuffer(C.Structure):
@@ -130,6 +131,7 @@ def scene_struct(scene) -> glint_scene:
     if len(scene.lights) > MAX_LIGHTS:
         raise ValueError(f"at most {MAX_LIGHTS} lights")
     s.n_lights = len(scene.lights)
+    s.eval_mode = {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
     for i, lt in enumerate(scene.lights):
         s.lights[i].kind = {"point": 0, "directional": 1}[lt.kind]
         s.lights[i].pos_or_dir[:] = [float(x) for x in lt.pos_or_dir]

@@ -195,6 +195,7 @@ static int validate_scene(const glint_scene* s) {
   if (s->max_ratio_level < 1 || s->max_ratio_level > 8) return GLINT_EINVAL;
   if (!(s->beta > 0.0f) || !isfinite(s->beta) || s->beta < 0x1p-20f) return GLINT_EINVAL;
   if (s->n_lights < 0 || s->n_lights > GLINT_MAX_LIGHTS) return GLINT_EINVAL;
+  if (s->eval_mode < 0 || s->eval_mode > 2) return GLINT_EINVAL;
   for (int l = 0; l < s->n_lights; ++l)
     if (s->lights[l].kind != 0 && s->lights[l].kind != 1) return GLINT_EINVAL;
   return GLINT_OK;
@@ -252,6 +253,7 @@ extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const gli
   if (rc) return rc;
   if (gb->width == 0 || gb->height == 0) return GLINT_OK;
   if (!out) return GLINT_EINVAL;
+  if (dbg && sc->eval_mode != 0) return GLINT_EINVAL;
   if (!aligned16(out)) return GLINT_EALIGN;
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));

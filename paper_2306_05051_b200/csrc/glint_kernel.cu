@@ -116,6 +116,59 @@ __device__ __forceinline__ void lattice(float P, float r, float psi, int K, Slot
   }
 }
 
+// S2 for the 160-draw ablation: all 10 prism vertices (2 LODs x pentagon),
+// linear in ts / tr, linear in a on the inner ring, hats at a = 0, 1/2, 1 on
+// the outer ring; coincident ring-0 vertices merged (reading R-29).
+__device__ __forceinline__ void lattice10(float P, float r, float psi, int K, int ls[10], int lr[10], int jo[10],
+                                          float w[10], uint32_t& flags) {
+  const uint32_t pb = __float_as_uint(P);
+  const int es = (int)((pb >> 23) & 255u) - 127;
+  const float ts = __uint_as_float((pb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+  int er;
+  float tr;
+  if (!(r >= 1.0f)) r = 1.0f;
+  const float rmax = pow2i(K);
+  if (r >= rmax) {
+    if (r > rmax) flags |= GLINT_FLAG_RATIO_CLAMPED;
+    er = K - 1;
+    tr = 1.0f;
+  } else {
+    const uint32_t rb = __float_as_uint(r);
+    er = (int)((rb >> 23) & 255u) - 127;
+    tr = __uint_as_float((rb & 0x7FFFFFu) | 0x3F800000u) - 1.0f;
+  }
+  const float A = psi * pow2i(er);
+  const float jf = floorf(A);
+  const float a = A - jf;
+  const int j = (int)jf;
+  const int nI = 1 << er, nO = 2 << er;
+  int vk[5] = {(er << 9) | j, (er << 9) | ((j + 1) & (nI - 1)), ((er + 1) << 9) | (2 * j),
+               ((er + 1) << 9) | (2 * j + 1), ((er + 1) << 9) | ((2 * j + 2) & (nO - 1))};
+  const float a2 = a + a, omt = 1.0f - tr;
+  const bool lo = a2 <= 1.0f;
+  float pw[5] = {omt * (1.0f - a), omt * a, tr * (lo ? 1.0f - a2 : 0.0f), tr * (lo ? a2 : 2.0f - a2),
+                 tr * (lo ? 0.0f : a2 - 1.0f)};
+#pragma unroll
+  for (int p = 0; p < 5; ++p)
+#pragma unroll
+    for (int q = p + 1; q < 5; ++q) {
+      const bool m = vk[p] == vk[q];
+      pw[p] = m ? pw[p] + pw[q] : pw[p];
+      pw[q] = m ? 0.0f : pw[q];
+    }
+#pragma unroll
+  for (int lv = 0; lv < 2; ++lv) {
+    const float sw = lv ? ts : 1.0f - ts;
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      ls[lv * 5 + p] = es + lv;
+      lr[lv * 5 + p] = vk[p] >> 9;
+      jo[lv * 5 + p] = vk[p] & 511;
+      w[lv * 5 + p] = sw * pw[p];
+    }
+  }
+}
+
 // fp32 Smith Lambda for the radiance path (R-21)
 // (tolerance path: MUFU-based approximations, |rel err| ~1e-7)
 __device__ __forceinline__ float smith_lambda(int kind, float ax2, float ay2, float wx, float wy, float wz) {
@@ -140,7 +193,7 @@ __shared__ float2 g_sCS[GLINT_NANG];
 // Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
 // pixel's output float4, `rec` its first debug record (DEBUG only).
 // ---------------------------------------------------------------------------
-template <bool DEBUG>
+template <bool DEBUG, int MODE>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
@@ -190,7 +243,17 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 
   // ---------------- S2: 4 grids + distribution weights, n_i = w_i N 2^ls
   Slot sl[4];
-  lattice(P, r, psi, sc.max_ratio_level, sl, flags);
+  constexpr int NGA = MODE == 2 ? 10 : 4;   // ablation grid list (MODE 1: the same 4 grids)
+  int als[NGA], alr[NGA], ajo[NGA];
+  float aw[NGA];
+  if (MODE == 2) {
+    lattice10(P, r, psi, sc.max_ratio_level, als, alr, ajo, aw, flags);
+    for (int i = 0; i < 4; ++i) { sl[i].ls = 0; sl[i].lr = 0; sl[i].jo = 0; sl[i].w = 0.0f; }
+  } else {
+    lattice(P, r, psi, sc.max_ratio_level, sl, flags);
+    if (MODE == 1)
+      for (int i = 0; i < 4; ++i) { als[i] = sl[i].ls; alr[i] = sl[i].lr; ajo[i] = sl[i].jo; aw[i] = sl[i].w; }
+  }
   const float ax = mat.x, ay = mat.y, N = mat.z, R = mat.w;
   float n[4];
 #pragma unroll
@@ -204,7 +267,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   float beta[12];
   uint32_t dlx[DEBUG ? 12 : 1], dly[DEBUG ? 12 : 1], dhs[DEBUG ? 12 : 1];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < (MODE == 0 ? 4 : 0); ++i) {
     const float2 cs = sCS[sl[i].jo << (8 - sl[i].lr)];
     const float xr = __fmaf_rn(cs.x, u, cs.y * v);
     const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
@@ -319,8 +382,46 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
     const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
     float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // A_j = sum_ik beta_ik c_ikj
+    if (MODE != 0) {
+      // ---- ablations: NGA grids x 4 bilinear texels x 4 nodes,
+      // everything per light (one grid at a time, rolled: small code)
+#pragma unroll 1
+      for (int g = 0; g < NGA; ++g) {
+        const float ng = aw[g] * (N * pow2i(als[g]));
+        const Gate gt = gate_params(ng, p, L2);
+        const uint32_t G = (gt.T << 9) - 1u;
+        const float capk = gt.T ? gt.cap : 0.0f;
+        const float2 cs = sCS[ajo[g] << (8 - alr[g])];
+        const float xr = __fmaf_rn(cs.x, u, cs.y * v);
+        const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
+        const float sxs = pow2half(-(als[g] + alr[g]));
+        const float gx = xr * sxs;
+        const float gy = yr * (sxs * pow2i(alr[g]));
+        const float fxs = floorf(gx), fys = floorf(gy);
+        const float fx = gx - fxs, fy = gy - fys;
+        const uint32_t ix = (uint32_t)(long long)fxs, iy = (uint32_t)(long long)fys;
+        const float bw[4] = {(1.0f - fx) * (1.0f - fy), fx * (1.0f - fy), (1.0f - fx) * fy, fx * fy};
+        const uint32_t key = ((uint32_t)als[g] & 511u) | ((uint32_t)alr[g] << 9) | ((uint32_t)ajo[g] << 13);
+        const uint32_t base = so + key * 0x9e3779b1U + ix * 0x8da6b343U + iy * 0xd8163841U;
+        const uint32_t lin[4] = {base, base + 0x8da6b343U, base + 0xd8163841U, base + (0x8da6b343U + 0xd8163841U)};
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t hC = (lowbias32(lin[k]) * 0x7feb352dU) ^ zero;
+#pragma unroll
+          for (int jn = 0; jn < 4; ++jn) {
+            uint32_t y = hC + kaC[jn];
+            y ^= y >> 15;
+            y *= 0x846ca68bU;
+            const uint32_t s16 = y >> 16;
+            const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
+            const float c = floorf(fminf(fmaxf(__fmaf_rn(gt.sigma, z, gt.m1), 1.0f), capk));
+            if (y <= G) A[jn] = __fmaf_rn(bw[k], c, A[jn]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < (MODE == 0 ? 4 : 0); ++i) {
       const Gate gt = gate_params(n[i], p, L2);
       // gate (y >> 9) < T  <=>  y <= T*512 - 1; T = 0 wraps to "always" but its
       // cap is forced to 0 so the count is 0 (same result, one compare)
@@ -387,7 +488,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 // which keeps its warps in the same code (instruction-cache friendly).
 // Otherwise the planes are read directly.
 // ---------------------------------------------------------------------------
-template <bool DEBUG, bool TMA>
+template <bool DEBUG, bool TMA, int MODE>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
   float* sZ = g_sZ;
   float2* sCS = g_sCS;
@@ -455,38 +556,42 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
         pos = __ldcs(prm.pos + gi); mat = __ldcs(prm.mat + gi);
         oi = (int64_t)y * prm.out_pitch + x;
       }
-      shade_pixel<DEBUG>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm,
+      shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm,
                          pos, mat, seed_h, inv_beta, prm.zero);
     }
   }
 }
 
-template <bool DEBUG, bool TMA>
+template <bool DEBUG, bool TMA, int MODE>
 static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream) {
   const size_t smem = TMA ? kSmemTma : kSmemTables;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  glint_eval_kernel<DEBUG, TMA><<<grid, kBlock, smem, stream>>>(prm);
+  glint_eval_kernel<DEBUG, TMA, MODE><<<grid, kBlock, smem, stream>>>(prm);
   return cudaGetLastError();
 }
 
 cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream) {
   const bool tma = (prm.pitch == prm.width) && (((uintptr_t)prm.duv | (uintptr_t)prm.uvm | (uintptr_t)prm.nrm |
                                                   (uintptr_t)prm.pos | (uintptr_t)prm.mat) % 16 == 0);
-  if (debug) return tma ? launch_t<true, true>(prm, grid, stream) : launch_t<true, false>(prm, grid, stream);
-  return tma ? launch_t<false, true>(prm, grid, stream) : launch_t<false, false>(prm, grid, stream);
+  if (debug) return tma ? launch_t<true, true, 0>(prm, grid, stream) : launch_t<true, false, 0>(prm, grid, stream);
+  switch (prm.sc.eval_mode) {
+    case 1: return tma ? launch_t<false, true, 1>(prm, grid, stream) : launch_t<false, false, 1>(prm, grid, stream);
+    case 2: return tma ? launch_t<false, true, 2>(prm, grid, stream) : launch_t<false, false, 2>(prm, grid, stream);
+    default: return tma ? launch_t<false, true, 0>(prm, grid, stream) : launch_t<false, false, 0>(prm, grid, stream);
+  }
 }
 
 cudaError_t occupancy_blocks_per_sm(int* out) {
-  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemTma);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true>, kBlock, kSmemTma);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true, 0>, kBlock, kSmemTma);
 }
 
 }  // namespace glint

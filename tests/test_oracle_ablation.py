@@ -1,0 +1,107 @@
+"""Pins for the evaluation-count ablations ("10 x 4 x 4 = 160",
+P:L758 "4 x 4 x 4 = 64", "4 x 3 x 4 = 48"): the naive 10-vertex
+prism distribution (reading R-29) and the bilinear spatial grid, against the
+same invariants as the tetrahedral / simplex versions."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2306_05051_b200 import synth
+
+
+def test_lattice10_partition_area_vertex(orc):
+    rng = np.random.default_rng(30)
+    for _ in range(5000):
+        P = float(np.float32(2.0 ** rng.uniform(-30, 10)))
+        r = float(np.float32(2.0 ** rng.uniform(0, 8.5)))
+        psi = float(np.float32(rng.random()))
+        ls, lr, jo, w, _ = orc.lattice10(P, r, psi)
+        w = np.array(w, np.float64)
+        assert w.min() >= -1e-7 and abs(w.sum() - 1) < 3e-6
+        assert abs(sum(wi * 2.0 ** a for wi, a in zip(w, ls)) - P) <= 4e-6 * P
+        keys = [(a, b, c) for a, b, c, wi in zip(ls, lr, jo, w) if wi > 0]
+        assert len(keys) == len(set(keys))
+    for e in (-12, 3):
+        for k in range(0, 8):
+            for j in range(0, 2 ** k, max(1, 2 ** k // 4)):
+                ls, lr, jo, w, _ = orc.lattice10(2.0 ** e, 2.0 ** k, j / 2 ** k)
+                nz = [(a, b, c) for a, b, c, wi in zip(ls, lr, jo, w) if wi != 0]
+                assert nz == [(e, k, j)]
+
+
+def test_lattice10_agrees_with_tetrahedra_on_linear_fields(orc):
+    """Both distributions reproduce the scale and ratio coordinates exactly
+    (sum of top-level weight = ts, of outer-ring weight = tr)."""
+    rng = np.random.default_rng(31)
+    for _ in range(3000):
+        er = int(rng.integers(0, 8))
+        r = float(np.float32(2.0 ** er * (1 + rng.random())))
+        if r >= 256:
+            continue
+        tr = r / 2.0 ** er - 1
+        P = float(np.float32(2.0 ** rng.uniform(-20, 5)))
+        e = math.floor(math.log2(P))
+        ts = P / 2.0 ** e - 1
+        psi = float(np.float32(rng.random()))
+        for fn in (orc.lattice, orc.lattice10):
+            ls, lr, jo, w, _ = fn(P, r, psi)
+            assert abs(sum(wi for wi, a in zip(w, ls) if a == e + 1) - ts) < 3e-6
+            assert abs(sum(wi for wi, b in zip(w, lr) if b == er + 1) - tr) < 3e-6
+
+
+def test_lattice10_isotropy_and_continuity(orc):
+    rng = np.random.default_rng(32)
+    nz = lambda L: sorted((a, b, c, round(wi, 6)) for a, b, c, wi in zip(*L[:4]) if wi != 0)
+    for _ in range(500):
+        P = float(np.float32(2.0 ** rng.uniform(-20, 5)))
+        ref = nz(orc.lattice10(P, 1.0, 0.0))
+        assert nz(orc.lattice10(P, 1.0, float(np.float32(rng.random())))) == ref
+    val = lambda a, b, c: ((a * 73856093 ^ b * 19349663 ^ c * 83492791) * 2654435761 % 2 ** 32) / 2 ** 32
+    f = lambda *x: sum(wi * val(a, b, c) for a, b, c, wi in zip(*orc.lattice10(*x)[:4]))
+    for _ in range(2000):
+        P = float(np.float32(2.0 ** rng.uniform(-20, 5)))
+        r = float(np.float32(2.0 ** rng.uniform(0.0, 7.99)))
+        psi = float(np.float32(rng.random()))
+        f0 = f(P, r, psi)
+        f1 = f(float(np.float32(P * (1 + 1e-6))), float(np.float32(r * (1 + 1e-6))), float(np.float32(psi + 1e-6)) % 1.0)
+        assert abs(f1 - f0) < 1e-3
+
+
+def test_bilinear_partition_and_vertices(orc):
+    rng = np.random.default_rng(33)
+    import ctypes as C
+    for _ in range(3000):
+        x, y = [float(np.float32(v)) for v in (rng.random(2) - 0.5) * 1000]
+        lx, ly, be = (C.c_int64 * 4)(), (C.c_int64 * 4)(), (C.c_float * 4)()
+        orc.lib().orc_bilinear.argtypes = [C.c_float, C.c_float, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                           C.POINTER(C.c_float)]
+        orc.lib().orc_bilinear(x, y, lx, ly, be)
+        be = np.array(list(be), np.float64)
+        assert be.min() >= 0 and abs(be.sum() - 1) < 1e-6
+        assert abs(float(np.dot(be, list(lx))) - x) < 1e-4 and abs(float(np.dot(be, list(ly))) - y) < 1e-4
+
+
+@pytest.mark.parametrize("draws", [64, 160])
+def test_ablations_have_the_same_expectation(orc, draws):
+    """All three distributions give an unbiased D_P with the exact sampler:
+    mean over seeds of C equals N P p (the draw count is the only change)."""
+    rng = np.random.default_rng(34)
+    fr = synth.c1("ggx", "az90")
+    gb = fr.gbuf.crop(0, 4, 0, 4)
+    # anisotropic footprint so the grids differ between modes
+    gb.duv[..., 0] = 0.011
+    gb.duv[..., 1] = 0.004
+    gb.duv[..., 2] = -0.002
+    gb.duv[..., 3] = 0.0061
+    gb.mat[..., 2] = 4e5
+    ms = []
+    for mode in (48, draws):
+        Cs = []
+        for sd in range(150):
+            sc = synth.SceneParams(**{**fr.scene.__dict__, "seed": 500 + sd, "draws": mode})
+            rgb, _, _ = orc.eval(gb, sc, sampler="exact", threads=1)
+            Cs.append(rgb[:, 0])
+        ms.append(np.mean(Cs, 0))
+    # same footprint and h in all 16 pixels: compare the pixel-averaged means
+    assert abs(ms[0].mean() / ms[1].mean() - 1) < 0.03, (ms[0].mean(), ms[1].mean())
