@@ -35,6 +35,8 @@ struct glint_ctx {
   float h_z[GLINT_ZQ];
   float h_cos[GLINT_NANG], h_sin[GLINT_NANG];
   std::atomic<int64_t> launches;
+  unsigned long long* d_sched;   // kSchedSlots x [tile counter, finished blocks], zeroed
+  std::atomic<int64_t> sched_next;
   // glint_eval_host staging (2 buffers x (5 planes + out)), grown on demand
   size_t stage_px;
   float4* d_stage[2][6];
@@ -114,6 +116,7 @@ extern "C" int glint_create(glint_ctx** out, int device) {
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
   c->launches = 0;
+  c->sched_next = 0;
   int rc = GLINT_OK;
   float2 cs[GLINT_NANG];
   glint_build_tables(c->h_z, c->h_cos, c->h_sin);
@@ -121,6 +124,8 @@ extern "C" int glint_create(glint_ctx** out, int device) {
   cudaError_t e = glint::occupancy_blocks_per_sm(&c->blocks_per_sm);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_z, sizeof(float) * GLINT_ZQ);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_cs, sizeof(float2) * GLINT_NANG);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sched, sizeof(unsigned long long) * 2 * glint::kSchedSlots);
+  if (e == cudaSuccess) e = cudaMemset(c->d_sched, 0, sizeof(unsigned long long) * 2 * glint::kSchedSlots);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_z, c->h_z, sizeof(float) * GLINT_ZQ, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_cs, cs, sizeof(float2) * GLINT_NANG, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -128,6 +133,7 @@ extern "C" int glint_create(glint_ctx** out, int device) {
     rc = GLINT_ECUDA;
     if (c->d_z) cudaFree(c->d_z);
     if (c->d_cs) cudaFree(c->d_cs);
+    if (c->d_sched) cudaFree(c->d_sched);
     delete c;
     c = nullptr;
   } else if (c->blocks_per_sm < 1) {
@@ -158,6 +164,7 @@ extern "C" int glint_destroy(glint_ctx* c) {
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   cudaFree(c->d_z);
   cudaFree(c->d_cs);
+  cudaFree(c->d_sched);
   cudaSetDevice(prev);
   delete c;
   return GLINT_OK;
@@ -216,6 +223,10 @@ static int validate_gbuffer(const glint_gbuffer* g, int64_t out_pitch) {
 
 static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc,
                                   void* out, int64_t out_pitch, glint_debug_rec* dbg) {
+  // a scheduler slot per launch (ring): concurrent launches on other streams
+  // use other slots; a slot is reused kSchedSlots launches later
+  glint_ctx* cm = const_cast<glint_ctx*>(c);
+  const int64_t slot = cm->sched_next.fetch_add(1) % glint::kSchedSlots;
   glint::KParams k;
   k.duv = (const float4*)gb->duv;
   k.uvm = (const float4*)gb->uvm;
@@ -231,6 +242,7 @@ static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, c
   k.pitch = gb->pitch;
   k.out_pitch = out_pitch;
   k.zero = 0u;
+  k.sched = c->d_sched + 2 * slot;
   k.sc = *sc;
   return k;
 }

@@ -525,15 +525,26 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
     bulk_g2s(tiles + (b * 5 + 4) * kTile, prm.mat + base, bytes, &bars[b]);
   };
 
-  int64_t t = blockIdx.x;
-  if (TMA && tid == 0 && t < n_tiles) issue(t, 0);
-  for (int it = 0; t < n_tiles; t += gridDim.x, ++it) {
+  // dynamic tile scheduling: the first tile is blockIdx.x, later ones are
+  // claimed from this launch's counter (balances per-tile cost variance and
+  // the tail); thread 0 claims the next tile while the block shades the
+  // current one and publishes it through shared memory.
+  __shared__ long long s_tile[2];
+  if (tid == 0) {
+    s_tile[0] = blockIdx.x;
+    if (TMA && (int64_t)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+  }
+  for (int it = 0;; ++it) {
     const int b = it & 1;
-    if (TMA) {
-      __syncthreads();   // the whole block is done reading buffer b^1 (iteration it-1)
-      if (tid == 0 && t + gridDim.x < n_tiles) issue(t + gridDim.x, b ^ 1);
-      mbar_wait(&bars[b], (uint32_t)(it >> 1) & 1u);
+    __syncthreads();   // buffer b^1 is free (iteration it-1 done) and s_tile[b] is visible
+    const int64_t t = s_tile[b];
+    if (t >= n_tiles) break;
+    if (tid == 0) {
+      const int64_t nt = (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull);
+      s_tile[b ^ 1] = nt;
+      if (TMA && nt < n_tiles) issue(nt, b ^ 1);
     }
+    if (TMA) mbar_wait(&bars[b], (uint32_t)(it >> 1) & 1u);
 #pragma unroll 1
     for (int q = 0; q < kPPT; ++q) {
       const int slot = q * kBlock + tid;
@@ -556,8 +567,18 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
         pos = __ldcs(prm.pos + gi); mat = __ldcs(prm.mat + gi);
         oi = (int64_t)y * prm.out_pitch + x;
       }
-      shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm, nrm,
-                         pos, mat, seed_h, inv_beta, prm.zero);
+      shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
+                               nrm, pos, mat, seed_h, inv_beta, prm.zero);
+    }
+  }
+  // every block made exactly one failing claim before leaving; the last block
+  // to finish resets this launch's counters for the next use of the slot
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&prm.sched[1], 1ull) == (unsigned long long)(gridDim.x - 1)) {
+      prm.sched[0] = 0ull;
+      prm.sched[1] = 0ull;
+      __threadfence();
     }
   }
 }

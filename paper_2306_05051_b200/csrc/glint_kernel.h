@@ -20,6 +20,7 @@ constexpr int kMinBlocks = GLINT_MIN_BLOCKS;   // resident blocks per SM the reg
 #endif
 constexpr int kPPT = GLINT_PPT;                 // pixels per thread per TMA tile
 constexpr int kTile = kBlock * kPPT;            // pixels per tile
+constexpr int kSchedSlots = 1024;               // per-context ring of per-launch scheduler counters
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
 constexpr size_t kSmemTables = 128;                            // dynamic part: 2 mbarriers (padded)
@@ -37,6 +38,8 @@ struct KParams {
   const float2* cstab;  // GLINT_NANG (cos, sin) pairs (device)
   int32_t width, height;
   int64_t pitch, out_pitch;
+  unsigned long long* sched;  // [tile counter, finished blocks] of this launch (dynamic tiles);
+                              // zero on entry, reset to zero by the last block
   uint32_t zero;        // always 0; XOR-ing pre-multiplied seeds with it stops ptxas
                         // from re-factoring hs*C1 + ka*C1 into (hs + ka)*C1 per draw
   glint_scene sc;
