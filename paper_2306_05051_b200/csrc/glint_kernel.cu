@@ -420,8 +420,16 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         }
       }
     }
+    // lanes shading this light (invalid pixels and lights below the horizon
+    // left earlier); warp votes below use this mask
+    const uint32_t am = __activemask();
 #pragma unroll
     for (int i = 0; i < (MODE == 0 ? 4 : 0); ++i) {
+      // a grid with no trials (zero distribution weight: ring-0 merges,
+      // isotropic footprints) or p = 0 draws only zeros; neighbouring pixels
+      // share their grid structure, so skip it when the whole warp agrees
+      // (results unchanged)
+      if (!DEBUG && !__any_sync(am, n[i] > 0.0f && p > 0.0f)) continue;
       const Gate gt = gate_params(n[i], p, L2);
       // gate (y >> 9) < T  <=>  y <= T*512 - 1; T = 0 wraps to "always" but its
       // cap is forced to 0 so the count is 0 (same result, one compare)
