@@ -85,6 +85,7 @@ def lib():
             L.orc_eval.restype = C.c_int
             L.orc_exp2.argtypes = [C.c_float]; L.orc_exp2.restype = C.c_float
             L.orc_rsqrt.argtypes = [C.c_float]; L.orc_rsqrt.restype = C.c_float
+            L.orc_rcp.argtypes = [C.c_float]; L.orc_rcp.restype = C.c_float
             L.orc_log2_1mp.argtypes = [C.c_float]; L.orc_log2_1mp.restype = C.c_float
             L.orc_atan2_turns.argtypes = [C.c_float, C.c_float]; L.orc_atan2_turns.restype = C.c_float
             L.orc_lowbias32.argtypes = [C.c_uint32]; L.orc_lowbias32.restype = C.c_uint32
@@ -207,6 +208,10 @@ def exp2(y: float) -> float:
 
 def rsqrt(x: float) -> float:
     return lib().orc_rsqrt(x)
+
+
+def rcp(x: float) -> float:
+    return lib().orc_rcp(x)
 
 
 def log2_1mp(p: float) -> float:

@@ -75,7 +75,9 @@ const float* orc_sintable(void) { orc_init(); return g_sin; }
  * of e^(f ln2) in Horner form, times 2^k. y < -125 -> 0. */
 float orc_exp2(float y) {
   if (!(y >= -125.0f)) return 0.0f;
-  float k = floorf(y + 0.5f);
+  /* k = rint(y) by the 1.5 2^23 magic number; 2^k from K's bits */
+  float K = y + 12582912.0f;
+  float k = K - 12582912.0f;
   float f = y - k;
   float q = 0x1.ffcbfcp-17f;           /* ln2^7/7! */
   q = fmaf(q, f, 0x1.430912p-13f);     /* ln2^6/6! */
@@ -85,7 +87,7 @@ float orc_exp2(float y) {
   q = fmaf(q, f, 0x1.ebfbe0p-3f);      /* ln2^2/2! */
   q = fmaf(q, f, 0x1.62e430p-1f);      /* ln2 */
   q = fmaf(q, f, 1.0f);
-  return q * pow2i((int32_t)k);
+  return q * u2f((f2u(K) - 0x4B3FFF81u) << 23);   /* 2^k: (K bits - 0x4B400000 + 127) << 23 */
 }
 
 /* atanh(s)/s = 1 + s^2/3 + s^4/5 + ... + s^14/15 (Horner in z = s^2) */
@@ -106,7 +108,7 @@ static float atanh_series(float s) {
  * otherwise 1 - p (exact) = 2^e m, m in [2/3, 4/3], log2 = e + 2 atanh((m-1)/(m+1))/ln2. */
 float orc_log2_1mp(float p) {
   if (p < 0.5f) {
-    float s = p / (2.0f - p);
+    float s = p * orc_rcp(2.0f - p);
     return -(atanh_series(s) * 0x1.715476p+1f); /* 2/ln2 */
   }
   float q = 1.0f - p;
@@ -114,7 +116,7 @@ float orc_log2_1mp(float p) {
   int32_t e = (int32_t)((b >> 23) & 255u) - 127;
   float m = u2f((b & 0x7FFFFFu) | 0x3F800000u); /* [1, 2) */
   if (m > 0x1.555556p+0f) { m = m * 0.5f; e = e + 1; }
-  float s = (m - 1.0f) / (m + 1.0f);
+  float s = (m - 1.0f) * orc_rcp(m + 1.0f);
   return fmaf(atanh_series(s), 0x1.715476p+1f, (float)e);
 }
 
@@ -125,10 +127,10 @@ float orc_atan2_turns(float y, float x) {
   float ax = fabsf(x), ay = fabsf(y);
   float mx = ax > ay ? ax : ay;
   float mn = ax > ay ? ay : ax;
-  if (mx == 0.0f) return 0.0f;
-  float t = mn / mx;
+  if (!(mx >= 0x1p-126f)) return 0.0f;   /* zero or subnormal: no direction */
+  float t = mn * orc_rcp(mx);
   float base = 0.0f;
-  if (t > 0x1.a8279ap-2f) { t = (t - 1.0f) / (t + 1.0f); base = 0.125f; }
+  if (t > 0x1.a8279ap-2f) { t = (t - 1.0f) * orc_rcp(t + 1.0f); base = 0.125f; }
   float z = t * t;
   float q = 0x1.32c69ep-7f;
   q = fmaf(q, z, -0x1.5bade6p-7f);
@@ -146,6 +148,17 @@ float orc_atan2_turns(float y, float x) {
   return a;
 }
 
+/* 1/x for normal x > 0: magic start 0x7ef311c7 - bits, three Newton steps
+ * e = 1 - x y, y <- y + y e (fma). Replaces IEEE division. */
+float orc_rcp(float x) {
+  float y = u2f(0x7ef311c7U - f2u(x));
+  float e;
+  e = fmaf(-x, y, 1.0f); y = fmaf(y, e, y);
+  e = fmaf(-x, y, 1.0f); y = fmaf(y, e, y);
+  e = fmaf(-x, y, 1.0f); y = fmaf(y, e, y);
+  return y;
+}
+
 /* 1/sqrt(x) for normal x > 0: magic-constant start 0x5f3759df - (bits >> 1),
  * then three Newton steps y <- y (3/2 - (x/2) y^2) with the fma written out
  * (DESIGN.md §4.2). Used to normalise directions. */
@@ -157,6 +170,11 @@ float orc_rsqrt(float x) {
   y = y * fmaf(-hx, y * y, 1.5f);
   return y;
 }
+
+/* sqrt(v) = v rsqrt(v) for normal v > 0, 0 otherwise (subnormals included:
+ * the Newton steps would overflow to inf * 0) (contract sqrt) */
+static float sqrt_c(float v) { return v >= 0x1p-126f ? v * orc_rsqrt(v) : 0.0f; }
+
 
 /* ---------------------------------------------------------------------- */
 /* Hash ("random seeds theta are distributed in a spatial and angular
@@ -195,10 +213,10 @@ int orc_footprint(const float duv[4], float* P, float* r, float* psi) {
   float b = dudx * dvdx + dudy * dvdy;
   float c = dvdx * dvdx + dvdy * dvdy;
   float hm = 0.5f * (a - c);
-  float disc = sqrtf(hm * hm + b * b);
+  float disc = sqrt_c(hm * hm + b * b);
   float lam = 0.5f * (a + c) + disc;
   *P = fabsf(det);
-  *r = lam / *P;
+  *r = lam * orc_rcp(*P);
   float at = orc_atan2_turns(2.0f * b, a - c);
   float ps = at < 0.0f ? at + 1.0f : at;
   if (ps >= 1.0f) ps = 0.0f;
@@ -438,7 +456,7 @@ void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, flo
   float nm1 = n - 1.0f;
   float mu = nm1 > 0.0f ? nm1 * p : 0.0f; /* Eq. 17 (R-4: n < 1 -> mu = 0) */
   float var = mu * (1.0f - p);
-  *sigma = var > 0.0f ? var * orc_rsqrt(var) : 0.0f; /* sqrt via the contract rsqrt */
+  *sigma = sqrt_c(var); /* contract sqrt */
   *m1 = 1.0f + mu;
   *cap = ceilf(n);
 }
@@ -477,18 +495,19 @@ static float exact_count(uint32_t h, float n, float p) {
 /* ---------------------------------------------------------------------- */
 float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz) {
   if (!(hz > 0.0f)) return 0.0f;
-  float X = hx * (1.0f / ax), Y = hy * (1.0f / ay);
+  float X = hx * orc_rcp(ax), Y = hy * orc_rcp(ay);
   float s2 = X * X + Y * Y;
   float hz2 = hz * hz;
   if (ndf_kind == 0) {
     float q = s2 + hz2;
-    return 1.0f / (q * q);
+    return orc_rcp(q * q);
   }
-  float e2 = s2 / hz2;
-  return orc_exp2(-(e2 * 0x1.715476p+0f)) / (hz2 * hz2);
+  float e2 = s2 * orc_rcp(hz2);
+  return orc_exp2(-(e2 * 0x1.715476p+0f)) * orc_rcp(hz2 * hz2);
 }
 
 /* fp32 contract vector helpers */
+float orc_rcp(float x);
 static float dot3f(const float a[3], const float b[3]) {
   return fmaf(a[2], b[2], fmaf(a[1], b[1], a[0] * b[0]));
 }
@@ -499,7 +518,7 @@ static void normalize3f(float v[3]) {
 /* Duff et al. 2017 branchless ONB from n (reading R-17) */
 static void onb_f(const float n[3], float t[3], float bt[3]) {
   float sgn = copysignf(1.0f, n[2]);
-  float a = -1.0f / (sgn + n[2]);
+  float a = -(sgn * orc_rcp(1.0f + fabsf(n[2])));   /* = -1/(sgn + nz) */
   float b = (n[0] * n[1]) * a;
   float nxxa = (n[0] * n[0]) * a;
   float nyya = (n[1] * n[1]) * a;

@@ -85,6 +85,7 @@ int orc_eval(const float* duv, const float* uvm, const float* nrm, const float* 
 /* contract primitives, exported for pin tests */
 float orc_exp2(float y);
 float orc_rsqrt(float x);
+float orc_rcp(float x);
 float orc_log2_1mp(float p);
 float orc_atan2_turns(float y, float x);
 uint32_t orc_lowbias32(uint32_t x);

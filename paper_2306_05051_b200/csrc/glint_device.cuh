@@ -24,8 +24,10 @@ __device__ __forceinline__ float pow2half(int e) {
 __device__ __forceinline__ float exp2c(float y) {
   const bool under = !(y >= -125.0f);   // -> 0 (select, branch-free)
   y = under ? 0.0f : y;
-  float k = floorf(y + 0.5f);
-  float f = y - k;
+  // k = rint(y) by the 1.5 2^23 magic number; 2^k from K's bits
+  const float K = y + 12582912.0f;
+  const float k = K - 12582912.0f;
+  const float f = y - k;
   float q = 0x1.ffcbfcp-17f;
   q = __fmaf_rn(q, f, 0x1.430912p-13f);
   q = __fmaf_rn(q, f, 0x1.5d87fep-10f);
@@ -34,10 +36,19 @@ __device__ __forceinline__ float exp2c(float y) {
   q = __fmaf_rn(q, f, 0x1.ebfbe0p-3f);
   q = __fmaf_rn(q, f, 0x1.62e430p-1f);
   q = __fmaf_rn(q, f, 1.0f);
-  // 2^k for integer-valued k in [-125, 0] without a float->int convert: the
-  // low bits of k + (2^23 + 127) are k + 127
-  const float p2 = __uint_as_float(__float_as_uint(k + 8388735.0f) << 23);
+  const float p2 = __uint_as_float((__float_as_uint(K) - 0x4B3FFF81u) << 23);   // 2^k
   return under ? 0.0f : q * p2;
+}
+
+// 1/x for normal x > 0: magic start + 3 Newton steps, branch-free;
+// replaces IEEE division on the decision path
+__device__ __forceinline__ float rcp_c(float x) {
+  float y = __uint_as_float(0x7ef311c7U - __float_as_uint(x));
+  float e;
+  e = __fmaf_rn(-x, y, 1.0f); y = __fmaf_rn(y, e, y);
+  e = __fmaf_rn(-x, y, 1.0f); y = __fmaf_rn(y, e, y);
+  e = __fmaf_rn(-x, y, 1.0f); y = __fmaf_rn(y, e, y);
+  return y;
 }
 
 // s * atanh(s)/s series to s^15 (Horner in s^2)
@@ -57,7 +68,7 @@ __device__ __forceinline__ float atanh_s(float s) {
 // log2(1 - p), p in (0, 1). DESIGN §4.2.
 __device__ __forceinline__ float log2_1mp(float p) {
   if (p < 0.5f) {
-    float s = p / (2.0f - p);
+    float s = p * rcp_c(2.0f - p);
     return -(atanh_s(s) * 0x1.715476p+1f);
   }
   float q = 1.0f - p;
@@ -65,7 +76,7 @@ __device__ __forceinline__ float log2_1mp(float p) {
   int e = (int)((b >> 23) & 255u) - 127;
   float m = __uint_as_float((b & 0x7FFFFFu) | 0x3F800000u);
   if (m > 0x1.555556p+0f) { m = m * 0.5f; e = e + 1; }
-  float s = (m - 1.0f) / (m + 1.0f);
+  float s = (m - 1.0f) * rcp_c(m + 1.0f);
   return __fmaf_rn(atanh_s(s), 0x1.715476p+1f, (float)e);
 }
 
@@ -74,10 +85,10 @@ __device__ __forceinline__ float atan2_turns(float y, float x) {
   float ax = fabsf(x), ay = fabsf(y);
   float mx = ax > ay ? ax : ay;
   float mn = ax > ay ? ay : ax;
-  if (mx == 0.0f) return 0.0f;
-  float t = mn / mx;
+  if (!(mx >= 0x1p-126f)) return 0.0f;   // zero or subnormal: no direction
+  float t = mn * rcp_c(mx);
   const bool red = t > 0x1.a8279ap-2f;   // reduce by 1/8 turn (select, branch-free)
-  const float tr = (t - 1.0f) / (t + 1.0f);
+  const float tr = (t - 1.0f) * rcp_c(t + 1.0f);
   t = red ? tr : t;
   const float base = red ? 0.125f : 0.0f;
   float z = t * t;
@@ -147,7 +158,7 @@ __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
   const float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
   const float var = mu * (1.0f - p);
   g.T = none ? 0u : T;
-  g.sigma = var > 0.0f ? var * rsqrt_c(var) : 0.0f;   // sqrt via the contract rsqrt
+  g.sigma = var >= 0x1p-126f ? var * rsqrt_c(var) : 0.0f;   // contract sqrt (subnormal -> 0)
   g.m1 = 1.0f + mu;
   g.cap = ceilf(n);
   return g;

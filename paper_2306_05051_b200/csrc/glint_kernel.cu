@@ -217,10 +217,11 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const float b = dudx * dvdx + dudy * dvdy;
     const float c = dvdx * dvdx + dvdy * dvdy;
     const float hm = 0.5f * (a - c);
-    const float disc = sqrtf(hm * hm + b * b);
+    const float dv = hm * hm + b * b;
+    const float disc = dv >= 0x1p-126f ? dv * rsqrt_c(dv) : 0.0f;   // contract sqrt (subnormal -> 0)
     const float lam = 0.5f * (a + c) + disc;
     P = fabsf(det);
-    r = lam / P;
+    r = lam * rcp_c(P);
     const float at = atan2_turns(2.0f * b, a - c);
     psi = at < 0.0f ? at + 1.0f : at;
     if (psi >= 1.0f) psi = 0.0f;
@@ -305,7 +306,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   float nx = nrm.x, ny = nrm.y, nz = nrm.z;
   normalize3(nx, ny, nz);
   const float sgn = copysignf(1.0f, nz);
-  const float oa = -1.0f / (sgn + nz);
+  const float oa = -(sgn * rcp_c(1.0f + fabsf(nz)));   // = -1/(sgn + nz)
   const float ob = (nx * ny) * oa;
   const float tx = 1.0f + sgn * ((nx * nx) * oa), ty = sgn * ob, tz = -(sgn * nx);
   const float bx = ob, by = sgn + (ny * ny) * oa, bz = -ny;
@@ -314,7 +315,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   else { wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2]; }
   normalize3(wix, wiy, wiz);
   const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
-  const float iax = 1.0f / ax, iay = 1.0f / ay;
+  const float iax = rcp_c(ax), iay = rcp_c(ay);
   // radiance-path constants (tolerance path: fast intrinsics allowed)
   // radiance-path constants, computed on first use (most pixels receive no
   // glint from any light: C = 0)
@@ -356,10 +357,10 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       const float hz2 = hz * hz;
       if (sc.ndf_kind == 0) {
         const float q = s2 + hz2;
-        ratio = 1.0f / (q * q);
+        ratio = rcp_c(q * q);
       } else {
-        const float e2 = s2 / hz2;
-        ratio = exp2c(-(e2 * 0x1.715476p+0f)) / (hz2 * hz2);
+        const float e2 = s2 * rcp_c(hz2);
+        ratio = exp2c(-(e2 * 0x1.715476p+0f)) * rcp_c(hz2 * hz2);
       }
     }
     float p = R * ratio;

@@ -34,6 +34,12 @@ def test_rsqrt_matches_libm(orc):
     assert abs(orc.rsqrt(4.0) - 0.5) <= 2 ** -24 and abs(orc.rsqrt(1.0) - 1.0) <= 2 ** -23
 
 
+def test_rcp_matches_libm(orc):
+    xs = np.concatenate([np.geomspace(1e-35, 1e35, 20001), np.linspace(1.0, 2.0, 20001)]).astype(np.float32)
+    worst = max(abs(orc.rcp(float(x)) * float(x) - 1.0) for x in xs)
+    assert worst < 2e-7, worst
+
+
 def test_log2_1mp_matches_libm(orc):
     ps = np.concatenate([np.geomspace(1e-38, 0.5, 3001), np.linspace(0.5, 1 - 1e-7, 3001)]).astype(np.float32)
     worst = 0.0

@@ -21,6 +21,19 @@ def test_footprint_closed_forms(orc):
     assert ok and r == 3.0 and abs(psi - 0.5) < 1e-7
 
 
+def test_footprint_subnormal_anisotropy_is_isotropic(orc):
+    """A near-isotropic footprint whose discriminant (a-c)^2/4 + b^2 is
+    subnormal (C2 at 90 deg elevation, DESIGN R-30) reads as exactly isotropic,
+    r = 1, with a finite orientation -- not the NaN the Newton steps of the
+    contract rsqrt would give on a subnormal input."""
+    s = np.float32(1.0691672e-02)
+    P, r, psi, ok = orc.footprint([s, 0.0, 3.85e-21, -s])
+    assert ok and r == 1.0 and 0.0 <= psi < 1.0
+    assert abs(P - float(s) * float(s)) <= 1e-6 * P
+    assert orc.atan2_turns(1e-45, 1e-45) == 0.0 and orc.atan2_turns(0.0, 0.0) == 0.0
+    assert orc.atan2_turns(-2e-40, 3e-39) == 0.0
+
+
 def test_footprint_vs_svd(orc):
     """P = s1 s2, r = s1/s2, psi = angle of the major singular vector / pi mod 1."""
     rng = np.random.default_rng(0)
