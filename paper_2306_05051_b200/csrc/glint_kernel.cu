@@ -186,8 +186,8 @@ __device__ __forceinline__ float smith_lambda(int kind, float ax2, float ay2, fl
 
 // shared tables at namespace scope: fixed shared-window offsets, so the
 // quantile lookup in the draw loop is a single LDS with an immediate base
-__shared__ float g_sZ[GLINT_ZQ];
-__shared__ float2 g_sCS[GLINT_NANG];
+__shared__ __align__(128) float g_sZ[GLINT_ZQ];
+__shared__ __align__(16) float2 g_sCS[GLINT_NANG];
 
 // ---------------------------------------------------------------------------
 // Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
@@ -490,29 +490,28 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 }
 
 // ---------------------------------------------------------------------------
-// The kernel: persistent blocks over 256-pixel tiles. TMA (contiguous
-// G-buffer, pitch == width): one thread issues the 5 bulk copies (5 x 4 KB)
-// of the block's next tile into the second buffer while the block shades the
-// current one (mbarrier-tracked, double-buffered); the block stays in step,
-// which keeps its warps in the same code (instruction-cache friendly).
-// Otherwise the planes are read directly.
+// The kernel: persistent blocks over kTile-pixel tiles, claimed dynamically
+// (the first tile is blockIdx.x, later ones come from this launch's counter:
+// balances per-tile cost variance and the tail). Warp 0 is the producer: one
+// tile ahead of itself it claims the next tile, waits until every warp has
+// released that ring stage, and (TMA: contiguous G-buffer, pitch == width)
+// issues the 5 bulk copies of the tile into it; a full mbarrier per stage
+// carries the tile id and the bytes, an empty mbarrier per stage counts the
+// warps done with it. No block-wide barrier inside the loop: a warp can run
+// up to kStages - 2 tiles ahead of the slowest one. Without TMA the planes
+// are read directly and the ring carries only tile ids.
 // ---------------------------------------------------------------------------
 template <bool DEBUG, bool TMA, int MODE>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
   float* sZ = g_sZ;
   float2* sCS = g_sCS;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(smem);   // tables loaded
+  uint64_t* full = tbar + 1;                             // [kStages] tile (and its bytes) ready
+  uint64_t* empty = full + kStages;                      // [kStages] kWarps arrivals: stage free
+  long long* s_tile = reinterpret_cast<long long*>(empty + kStages);   // [kStages] tile ids
   float4* tiles = reinterpret_cast<float4*>(smem + kSmemTables);
-  const int tid = threadIdx.x;
-  for (int i = tid; i < GLINT_ZQ; i += kBlock) sZ[i] = prm.ztab[i];
-  for (int i = tid; i < GLINT_NANG; i += kBlock) sCS[i] = prm.cstab[i];
-  if (TMA && tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   const glint_scene& sc = prm.sc;
   const int64_t n_pix = (int64_t)prm.width * prm.height;
@@ -521,39 +520,55 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   const uint32_t seed_h = lowbias32(sc.seed);
   const bool flat_out = prm.out_pitch == prm.width;
 
-  auto issue = [&](int64_t t, int b) {   // one thread: 5 bulk copies of tile t into buffer b
-    const int64_t base = t * kTile;
-    const int64_t cnt = (n_pix - base) < kTile ? (n_pix - base) : kTile;
-    const uint32_t bytes = (uint32_t)cnt * 16u;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&bars[b], 5u * bytes);
-    bulk_g2s(tiles + (b * 5 + 0) * kTile, prm.duv + base, bytes, &bars[b]);
-    bulk_g2s(tiles + (b * 5 + 1) * kTile, prm.uvm + base, bytes, &bars[b]);
-    bulk_g2s(tiles + (b * 5 + 2) * kTile, prm.nrm + base, bytes, &bars[b]);
-    bulk_g2s(tiles + (b * 5 + 3) * kTile, prm.pos + base, bytes, &bars[b]);
-    bulk_g2s(tiles + (b * 5 + 4) * kTile, prm.mat + base, bytes, &bars[b]);
+  auto issue = [&](int64_t t, int b) {   // one thread: tile t into stage b (or just its id)
+    if (TMA && t < n_tiles) {
+      const int64_t base = t * kTile;
+      const int64_t cnt = (n_pix - base) < kTile ? (n_pix - base) : kTile;
+      const uint32_t bytes = (uint32_t)cnt * 16u;
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&full[b], 5u * bytes);
+      bulk_g2s(tiles + (b * 5 + 0) * kTile, prm.duv + base, bytes, &full[b]);
+      bulk_g2s(tiles + (b * 5 + 1) * kTile, prm.uvm + base, bytes, &full[b]);
+      bulk_g2s(tiles + (b * 5 + 2) * kTile, prm.nrm + base, bytes, &full[b]);
+      bulk_g2s(tiles + (b * 5 + 3) * kTile, prm.pos + base, bytes, &full[b]);
+      bulk_g2s(tiles + (b * 5 + 4) * kTile, prm.mat + base, bytes, &full[b]);
+    } else {
+      mbar_arrive(&full[b]);
+    }
   };
 
-  // dynamic tile scheduling: the first tile is blockIdx.x, later ones are
-  // claimed from this launch's counter (balances per-tile cost variance and
-  // the tail); thread 0 claims the next tile while the block shades the
-  // current one and publishes it through shared memory.
-  __shared__ long long s_tile[2];
   if (tid == 0) {
+    mbar_init(tbar, 1);
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+    fence_mbar_init();
+    // tables: one bulk copy each (16 KB quantiles, 2 KB orientations)
+    mbar_arrive_expect_tx(tbar, (uint32_t)(kSmemZ + kSmemCS));
+    bulk_g2s(sZ, prm.ztab, (uint32_t)kSmemZ, tbar);
+    bulk_g2s(sCS, prm.cstab, (uint32_t)kSmemCS, tbar);
     s_tile[0] = blockIdx.x;
-    if (TMA && (int64_t)blockIdx.x < n_tiles) issue(blockIdx.x, 0);
+    issue(blockIdx.x, 0);
   }
+  __syncthreads();   // barriers initialised (the only block-wide barrier)
+  mbar_wait(tbar, 0u);
+
+  bool more = (int64_t)blockIdx.x < n_tiles;   // producer state (warp 0): claims not yet exhausted
   for (int it = 0;; ++it) {
-    const int b = it & 1;
-    __syncthreads();   // buffer b^1 is free (iteration it-1 done) and s_tile[b] is visible
-    const int64_t t = s_tile[b];
-    if (t >= n_tiles) break;
-    if (tid == 0) {
-      const int64_t nt = (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull);
-      s_tile[b ^ 1] = nt;
-      if (TMA && nt < n_tiles) issue(nt, b ^ 1);
+    const int s = it % kStages;
+    if (warp == 0 && more) {
+      // produce iteration it + 1: its stage was last consumed at it + 1 - kStages
+      const int s1 = (it + 1) % kStages;
+      if (it + 1 >= kStages) mbar_wait(&empty[s1], (uint32_t)((it + 1) / kStages - 1) & 1u);
+      if (lane == 0) {
+        const int64_t nt = (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull);
+        s_tile[s1] = nt;
+        issue(nt, s1);
+        more = nt < n_tiles;
+      }
+      more = __shfl_sync(0xffffffffu, more, 0);
     }
-    if (TMA) mbar_wait(&bars[b], (uint32_t)(it >> 1) & 1u);
+    mbar_wait(&full[s], (uint32_t)(it / kStages) & 1u);
+    const int64_t t = s_tile[s];
+    if (t >= n_tiles) break;
 #pragma unroll 1
     for (int q = 0; q < kPPT; ++q) {
       const int slot = q * kBlock + tid;
@@ -562,7 +577,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       float4 duv, uvm, nrm, pos, mat;
       int64_t oi = idx;
       if (TMA) {
-        const float4* tb = tiles + b * 5 * kTile + slot;
+        const float4* tb = tiles + s * 5 * kTile + slot;
         duv = tb[0]; uvm = tb[kTile]; nrm = tb[2 * kTile]; pos = tb[3 * kTile]; mat = tb[4 * kTile];
         if (!flat_out) {
           const uint32_t y = (uint32_t)idx / (uint32_t)prm.width;
@@ -579,9 +594,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
                                nrm, pos, mat, seed_h, inv_beta, prm.zero);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
   }
-  // every block made exactly one failing claim before leaving; the last block
-  // to finish resets this launch's counters for the next use of the slot
+  // every block's producer made exactly one failing claim (or none) before
+  // leaving; the last block to finish resets this launch's counters
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(&prm.sched[1], 1ull) == (unsigned long long)(gridDim.x - 1)) {

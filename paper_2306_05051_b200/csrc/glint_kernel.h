@@ -20,11 +20,17 @@ constexpr int kMinBlocks = GLINT_MIN_BLOCKS;   // resident blocks per SM the reg
 #endif
 constexpr int kPPT = GLINT_PPT;                 // pixels per thread per TMA tile
 constexpr int kTile = kBlock * kPPT;            // pixels per tile
+#ifndef GLINT_STAGES
+#define GLINT_STAGES 2
+#endif
+constexpr int kStages = GLINT_STAGES;           // G-buffer tile ring (full/empty mbarrier pairs)
+constexpr int kWarps = kBlock / 32;
 constexpr int kSchedSlots = 1024;               // per-context ring of per-launch scheduler counters
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
-constexpr size_t kSmemTables = 128;                            // dynamic part: 2 mbarriers (padded)
-constexpr size_t kSmemTma = kSmemTables + 2 * 5 * (size_t)kTile * 16;  // + 2 x 5 planes x kTile float4
+constexpr size_t kSmemTables = 256;    // dynamic part: table + 2 x kStages mbarriers, tile ids (padded)
+static_assert(8 * (1 + 2 * kStages) + 8 * kStages <= kSmemTables, "barrier area");
+constexpr size_t kSmemTma = kSmemTables + (size_t)kStages * 5 * kTile * 16;  // + kStages x 5 planes x kTile float4
 
 struct KParams {
   const float4* duv;
