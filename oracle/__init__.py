@@ -113,6 +113,13 @@ def lib():
             L.orc_smith_g2.restype = C.c_double
             L.orc_schlick.argtypes = [C.c_double, C.c_double]
             L.orc_schlick.restype = C.c_double
+            f16 = C.c_float * 16
+            L.orc_zk_probes.argtypes = [C.c_float * 4, C.c_float, C.c_float, f16, f16, fp, C.POINTER(C.c_uint32)]
+            L.orc_zk_probes.restype = C.c_int
+            L.orc_zk_lod.argtypes = [C.c_float, C.POINTER(C.c_int32), fp]
+            L.orc_zk_lod.restype = None
+            L.orc_zk_count.argtypes = [C.c_uint32, C.c_float, C.c_float]
+            L.orc_zk_count.restype = C.c_float
             L.orc_init()
             _lib = L
     return _lib
@@ -132,6 +139,14 @@ def sintable() -> np.ndarray:
 
 
 # --------------------------------------------------------------------------- scene
+def eval_mode_of(scene) -> int:
+    """0/1/2 = the method with 48 draws or its 64/160-draw ablations; 3 = the
+    Zirr & Kaplanyan-style baseline (scene.method == "zk")."""
+    if getattr(scene, "method", "ours") == "zk":
+        return 3
+    return {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
+
+
 def scene_struct(scene, sampler: str = "gated") -> _Scene:
     """Marshal a scene description (any object with the SceneParams fields)."""
     s = _Scene()
@@ -146,7 +161,7 @@ def scene_struct(scene, sampler: str = "gated") -> _Scene:
         raise ValueError("too many lights")
     s.n_lights = len(scene.lights)
     s.sampler = {"gated": 0, "exact": 1}[sampler]
-    s.eval_mode = {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
+    s.eval_mode = eval_mode_of(scene)
     for i, lt in enumerate(scene.lights):
         s.lights[i].kind = 0 if lt.kind == "point" else 1
         s.lights[i].pos_or_dir[:] = [float(x) for x in lt.pos_or_dir]
@@ -286,3 +301,22 @@ def smith_g2(ndf: str, ax, ay, wi_local, wo_local) -> float:
 
 def schlick(f0: float, cos_t: float) -> float:
     return lib().orc_schlick(f0, cos_t)
+
+
+# --------------------------------------------------------------------------- ZK baseline pieces
+def zk_probes(duv, u: float, v: float):
+    """(n, uk[n], vk[n], probe area, flags) of the ZK baseline's footprint probes."""
+    uk, vk = (C.c_float * 16)(), (C.c_float * 16)()
+    A, fl = C.c_float(), C.c_uint32(0)
+    n = lib().orc_zk_probes((C.c_float * 4)(*[float(x) for x in duv]), u, v, uk, vk, C.byref(A), C.byref(fl))
+    return n, list(uk)[:n], list(vk)[:n], A.value, fl.value
+
+
+def zk_lod(A: float):
+    k, t = C.c_int32(), C.c_float()
+    lib().orc_zk_lod(A, C.byref(k), C.byref(t))
+    return k.value, t.value
+
+
+def zk_count(w: int, nt: float, p: float) -> int:
+    return int(lib().orc_zk_count(w & 0xFFFFFFFF, nt, p))

@@ -561,6 +561,138 @@ double orc_schlick(double f0, double cos_t) {
 }
 
 /* ---------------------------------------------------------------------- */
+/* Zirr & Kaplanyan-style baseline (eval_mode 3), from the
+ * paper's description of that method only (their code is not available):
+ *  - anisotropic footprints are filtered by probing: "the counting law needs
+ *    to be manually evaluated for each texel under the pixel footprint"
+ *    (P:L188), with the anisotropy capped at x16 beyond which the footprint
+ *    grows isotropically;
+ *  - LOD levels whose cells quadruple in area, two at a time, blended
+ *    by OUTPUT: b = mix(b(N P_top, p), b(N P_bottom, p), w) (Eq. 7);
+ *  - random seeds on a spatial and an angular grid, evaluations bilinearly
+ *    interpolated;
+ *  - the classical binomial: floor(N(theta0; mu, sigma^2)) if N p > 5, else the
+ *    sum of N Bernoulli trials H(theta_k - p), looped up to N = 16 (Eq. 15,
+ *    P:L975-983).
+ * The readings that make this concrete are DESIGN.md R-31..R-36. */
+/* ---------------------------------------------------------------------- */
+
+/* R-31/R-32: probes along the footprint's major axis. From M = J J^T (S1's
+ * a, b, c, lambda): n = min(ceil(r), 16) probes, each of area P / n, centred
+ * at uv + ((2k + 1 - n) (1/2) / n) sigma_max e, e = unit major-axis direction
+ * (the eigenvector of M for lambda, from its better-conditioned row), and
+ * sigma_max = sqrt(lambda). Returns n; flags RATIO_CLAMPED if ceil(r) > 16. */
+int orc_zk_probes(const float duv[4], float u, float v, float uk[16], float vk[16], float* area,
+                  uint32_t* flags) {
+  float dudx = duv[0], dvdx = duv[1], dudy = duv[2], dvdy = duv[3];
+  float det = dudx * dvdy - dvdx * dudy;
+  float a = dudx * dudx + dudy * dudy;
+  float b = dudx * dvdx + dudy * dvdy;
+  float c = dvdx * dvdx + dvdy * dvdy;
+  float hm = 0.5f * (a - c);
+  float disc = sqrt_c(hm * hm + b * b);
+  float lam = 0.5f * (a + c) + disc;
+  float P = fabsf(det);
+  float r = lam * orc_rcp(P);
+  float ex = a >= c ? lam - c : b;
+  float ey = a >= c ? b : lam - a;
+  float l2 = ex * ex + ey * ey;
+  if (l2 >= 0x1p-126f) { float il = orc_rsqrt(l2); ex = ex * il; ey = ey * il; }
+  else { ex = 1.0f; ey = 0.0f; }
+  float cr = ceilf(r);
+  if (cr > 16.0f) *flags |= ORC_FLAG_RATIO_CLAMPED;
+  int n = cr >= 16.0f ? 16 : (cr >= 1.0f ? (int)cr : 1);
+  float rn = orc_rcp((float)n);
+  *area = P * rn;
+  float smax = sqrt_c(lam);
+  float q = 0.5f * rn;
+  for (int k = 0; k < n; ++k) {
+    float off = ((float)(2 * k + 1 - n) * q) * smax;
+    uk[k] = fmaf(off, ex, u);
+    vk[k] = fmaf(off, ey, v);
+  }
+  return n;
+}
+
+/* R-33: LOD pair of a probe of area A. Level l has cells of side 2^l (area
+ * 4^l); A = 4^kz (1 + t), t in [0, 3) from A's exponent bits (kz = floor(e/2));
+ * the output mix puts weight wt = t/3 on level kz + 1 and 1 - wt on kz, so
+ * that (1 - wt) 4^kz + wt 4^(kz+1) = A (Eq. 7 with E[b] = N A p). */
+void orc_zk_lod(float A, int32_t* kz, float* t) {
+  int32_t e = (int32_t)((f2u(A) >> 23) & 255u) - 127;
+  int32_t k = e >> 1;                   /* floor(e / 2) */
+  *kz = k;
+  *t = A * pow2i(-2 * k) - 1.0f;       /* exact: power-of-2 scaling, result in [0, 3) */
+}
+
+/* R-34: the classical binomial of Eq. 15 for one (texel, angular node) with
+ * nt = N 4^l trials and draw word w: Gaussian floor(mu + sigma z) clamped to
+ * [0, ceil(nt)] (z = Z[(w >> 2) & 4095], mu = nt p, sigma = sqrt(nt p (1-p)))
+ * when nt p > 5 or nt > 16; otherwise floor(nt) Bernoulli trials
+ * theta_k = lowbias32(w + k 0x9e3779b9) >> 8 < ceil(p 2^24) plus one
+ * fractional trial (k = 16) with probability frac(nt) p (R-35), so that
+ * E = nt p exactly in the looped regime. */
+float orc_zk_count(uint32_t w, float nt, float p) {
+  orc_init();
+  float np = nt * p;
+  if (np > 5.0f || nt > 16.0f) {
+    float sg = sqrt_c(np * (1.0f - p));
+    float z = g_z[(w >> 2) & (ORC_ZQ - 1)];
+    float x = fmaf(sg, z, np);
+    float cap = ceilf(nt);
+    x = x < 0.0f ? 0.0f : x;
+    x = x > cap ? cap : x;
+    return floorf(x);
+  }
+  float nf = floorf(nt);
+  uint32_t Tp = (uint32_t)ceilf(p * 0x1p24f);
+  uint32_t Tf = (uint32_t)ceilf(((nt - nf) * p) * 0x1p24f);
+  int c = 0;
+  for (int k = 0; k < (int)nf; ++k)
+    if ((orc_lowbias32(w + (uint32_t)k * 0x9e3779b9U) >> 8) < Tp) ++c;
+  if ((orc_lowbias32(w + 16u * 0x9e3779b9U) >> 8) < Tf) ++c;
+  return (float)c;
+}
+
+/* R-36: texel seed of the ZK random texture (its own key domain): level l,
+ * texel (lx, ly) of the side-2^l grid, object/seed word so. */
+static uint32_t zk_texel_seed(uint32_t so, int32_t l, int64_t lx, int64_t ly) {
+  return orc_lowbias32(so + (uint32_t)l * 0x5bd1e995U + (uint32_t)lx * 0x8da6b343U +
+                       (uint32_t)ly * 0xd8163841U + 0x68e31da4U);
+}
+
+/* blended count C of one pixel-light (fp64 weights, exact integer counts) */
+static double zk_blend(int npr, const float uk[16], const float vk[16], float A, uint32_t so,
+                       float N, float p, const uint32_t ka[4], const double vj[4]) {
+  int32_t kz; float t;
+  orc_zk_lod(A, &kz, &t);
+  double wt = (double)t / 3.0;
+  double C = 0.0;
+  for (int k = 0; k < npr; ++k) {
+    for (int lev = 0; lev < 2; ++lev) {
+      int32_t l = kz + lev;
+      double wl = lev ? wt : 1.0 - wt;
+      float nt = N * pow2i(2 * l);
+      if (!(nt <= 0x1p64f)) nt = 0x1p64f;
+      float s = pow2i(-l);
+      float gx = fmaf(uk[k], s, -0.5f), gy = fmaf(vk[k], s, -0.5f);
+      float fxs = floorf(gx), fys = floorf(gy);
+      double fx = (double)(gx - fxs), fy = (double)(gy - fys);
+      int64_t ix = (int64_t)fxs, iy = (int64_t)fys;
+      double bq[4] = {(1.0 - fx) * (1.0 - fy), fx * (1.0 - fy), (1.0 - fx) * fy, fx * fy};
+      for (int q = 0; q < 4; ++q) {
+        uint32_t hz = zk_texel_seed(so, l, ix + (q & 1), iy + (q >> 1));
+        double Cq = 0.0;
+        for (int jn = 0; jn < 4; ++jn)
+          Cq += vj[jn] * (double)orc_zk_count(orc_lowbias32(hz + ka[jn]), nt, p);
+        C += wl * bq[q] * Cq;
+      }
+    }
+  }
+  return C;
+}
+
+/* ---------------------------------------------------------------------- */
 /* S0..S9 for one pixel                                                     */
 /* ---------------------------------------------------------------------- */
 static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4],
@@ -586,11 +718,16 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
    * weights; n_i = w_i N 2^ls_i (R-14: "N_i proportional to its area",
    * P:L633). Ablation mode 2 (160 draws) uses all 10 prism vertices (R-29). */
   const int mode = sc->eval_mode;
-  const int NG = mode == 2 ? 10 : 4;          /* grids */
+  const int NG = mode == 3 ? 0 : (mode == 2 ? 10 : 4);   /* grids (mode 3: ZK probes instead) */
   const int NS = mode == 0 ? 3 : 4;           /* spatial texels per grid */
   int32_t ls[10], lr[10], jo[10];
   float w[10], n[10];
-  if (mode == 2) orc_lattice10(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
+  float zuk[16], zvk[16], zA = 0.0f;
+  int znp = 0;
+  if (mode == 3) {
+    znp = orc_zk_probes(duv, u, v, zuk, zvk, &zA, &flags);
+    for (int i = 0; i < 4; ++i) { ls[i] = lr[i] = jo[i] = 0; w[i] = 0.0f; }
+  } else if (mode == 2) orc_lattice10(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
   else orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
   float N = mat[2], R = mat[3], ax = mat[0], ay = mat[1];
   for (int i = 0; i < NG; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
@@ -691,7 +828,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
 
     /* S6 + S7 + S8: 4 grids x 3 spatial x 4 angular = 48 draws
      * (ablations: 4 x 4 x 4 = 64; 10 x 4 x 4 = 160) */
-    double C = 0.0;
+    double C = mode == 3 ? zk_blend(znp, zuk, zvk, zA, so, N, p, ka, vj) : 0.0;
     for (int i = 0; i < NG; ++i) {
       uint32_t T; float sig, m1, cap;
       orc_gate_params(n[i], p, &T, &sig, &m1, &cap);
@@ -749,7 +886,7 @@ int orc_eval(const float* duv, const float* uvm, const float* nrm, const float* 
              uint32_t* flags, orc_rec* rec) {
   orc_init();
   if (sc->n_lights < 0 || sc->n_lights > ORC_MAX_LIGHTS) return -1;
-  if (sc->eval_mode < 0 || sc->eval_mode > 2) return -1;
+  if (sc->eval_mode < 0 || sc->eval_mode > 3) return -1;
   if (rec && sc->eval_mode != 0) return -1;   /* debug records describe the 48-draw path */
   for (int64_t i = 0; i < n; ++i)
     eval_pixel(duv + 4 * i, uvm + 4 * i, nrm + 4 * i, pos + 4 * i, mat + 4 * i, sc,

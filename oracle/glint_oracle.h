@@ -47,7 +47,8 @@ typedef struct {
   int32_t sampler;         /* 0 = gated Gaussian (Eq. 18), 1 = exact Bernoulli sum (tests) */
   int32_t eval_mode;       /* draws per pixel-light: 0 = 48 (tetrahedra x simplex x angular),
                               1 = 64 (tetrahedra x bilinear x angular), 2 = 160 (10 prism
-                              vertices x bilinear x angular) -- P:L749, L758, L928 */
+                              vertices x bilinear x angular) -- P:L749, L758, L928;
+                              3 = Zirr & Kaplanyan-style baseline */
   int32_t pad_[2];
   orc_light lights[ORC_MAX_LIGHTS];
 } orc_scene;
@@ -103,4 +104,8 @@ float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap);
 float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz);
 double orc_smith_g2(int32_t kind, double ax, double ay, const double wi_l[3], const double wo_l[3]);
 double orc_schlick(double f0, double cos_t);
+int orc_zk_probes(const float duv[4], float u, float v, float uk[16], float vk[16], float* area,
+                  uint32_t* flags);
+void orc_zk_lod(float A, int32_t* kz, float* t);
+float orc_zk_count(uint32_t w, float nt, float p);
 #endif

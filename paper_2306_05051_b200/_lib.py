@@ -131,7 +131,7 @@ def scene_struct(scene) -> glint_scene:
     if len(scene.lights) > MAX_LIGHTS:
         raise ValueError(f"at most {MAX_LIGHTS} lights")
     s.n_lights = len(scene.lights)
-    s.eval_mode = {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
+    s.eval_mode = 3 if getattr(scene, "method", "ours") == "zk" else {48: 0, 64: 1, 160: 2}[int(getattr(scene, "draws", 48))]
     for i, lt in enumerate(scene.lights):
         s.lights[i].kind = {"point": 0, "directional": 1}[lt.kind]
         s.lights[i].pos_or_dir[:] = [float(x) for x in lt.pos_or_dir]

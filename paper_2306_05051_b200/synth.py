@@ -60,6 +60,7 @@ class SceneParams:
     view: Tuple[float, float, float] = (0.0, 0.0, 1.0)
     lights: List[Light] = field(default_factory=list)
     draws: int = 48                         # 48 (the paper's method); 64 / 160 = its ablations
+    method: str = "ours"                    # "ours" | "zk" (Zirr & Kaplanyan-style baseline)
 
 
 @dataclass
