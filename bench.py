@@ -174,6 +174,7 @@ def run_reference(args):
     frames, desc = make_frames(args.config, "cpu", seed=1)
     for fr in frames:
         fr.scene.draws = args.draws
+        fr.scene.method = args.method
     stride = 64 if args.config == "C2" else 256
     subs = oracle_sample(frames, stride)
     cores = host_cores()
@@ -223,8 +224,11 @@ def run_ours(args):
     frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank)
     for fr in frames:
         fr.scene.draws = args.draws
+        fr.scene.method = args.method
     if args.draws != 48:
         desc += f"; ABLATION: {args.draws} draws per pixel-light (P:L749/L758)"
+    if args.method == "zk":
+        desc += "; BASELINE: Zirr & Kaplanyan-style path (DESIGN.md section 10), not the paper's method"
     tot_px, valid_px, evals = count_evals(frames)
     outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
     stream = torch.cuda.current_stream(dev)
@@ -360,6 +364,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--method", default="ours", choices=["ours", "zk"],
+                    help="ours = the paper's method; zk = the Zirr & Kaplanyan-style baseline (eval_mode 3)")
     ap.add_argument("--draws", type=int, default=48, choices=[48, 64, 160],
                     help="draws per pixel-light: 48 = the method; 64 / 160 = its section-6 ablations")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -202,7 +202,7 @@ static int validate_scene(const glint_scene* s) {
   if (s->max_ratio_level < 1 || s->max_ratio_level > 8) return GLINT_EINVAL;
   if (!(s->beta > 0.0f) || !isfinite(s->beta) || s->beta < 0x1p-20f) return GLINT_EINVAL;
   if (s->n_lights < 0 || s->n_lights > GLINT_MAX_LIGHTS) return GLINT_EINVAL;
-  if (s->eval_mode < 0 || s->eval_mode > 2) return GLINT_EINVAL;
+  if (s->eval_mode < 0 || s->eval_mode > 3) return GLINT_EINVAL;
   for (int l = 0; l < s->n_lights; ++l)
     if (s->lights[l].kind != 0 && s->lights[l].kind != 1) return GLINT_EINVAL;
   return GLINT_OK;

@@ -210,6 +210,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   }
   // ---------------- S1: footprint (R-7, R-8)
   float P = 0.0f, r = 0.0f, psi = 0.0f;
+  float zex = 1.0f, zey = 0.0f, zsmax = 0.0f;   // MODE 3: major axis, sigma_max (R-32)
   if (ok) {
     const float dudx = duv.x, dvdx = duv.y, dudy = duv.z, dvdy = duv.w;
     const float det = dudx * dvdy - dvdx * dudy;
@@ -229,6 +230,22 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       flags = GLINT_FLAG_DEGENERATE;
       ok = false;
     }
+    if (MODE == 3) {
+      float ex = a >= c ? lam - c : b;
+      float ey = a >= c ? b : lam - a;
+      const float l2 = ex * ex + ey * ey;
+      if (l2 >= 0x1p-126f) {
+        const float il = rsqrt_c(l2);
+        ex = ex * il;
+        ey = ey * il;
+      } else {
+        ex = 1.0f;
+        ey = 0.0f;
+      }
+      zex = ex;
+      zey = ey;
+      zsmax = lam >= 0x1p-126f ? lam * rsqrt_c(lam) : 0.0f;
+    }
   }
   if (!ok) {
     __stcs(outp, make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(flags)));
@@ -247,7 +264,17 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   constexpr int NGA = MODE == 2 ? 10 : 4;   // ablation grid list (MODE 1: the same 4 grids)
   int als[NGA], alr[NGA], ajo[NGA];
   float aw[NGA];
-  if (MODE == 2) {
+  int znp = 1;            // MODE 3: probes, their area and half-step (R-31, R-32)
+  float zA = 0.0f, zq = 0.0f;
+  if (MODE == 3) {
+    for (int i = 0; i < 4; ++i) { sl[i].ls = 0; sl[i].lr = 0; sl[i].jo = 0; sl[i].w = 0.0f; }
+    const float cr = ceilf(r);
+    if (cr > 16.0f) flags |= GLINT_FLAG_RATIO_CLAMPED;
+    znp = cr >= 16.0f ? 16 : (cr >= 1.0f ? (int)cr : 1);
+    const float rn = rcp_c((float)znp);
+    zA = P * rn;
+    zq = 0.5f * rn;
+  } else if (MODE == 2) {
     lattice10(P, r, psi, sc.max_ratio_level, als, alr, ajo, aw, flags);
     for (int i = 0; i < 4; ++i) { sl[i].ls = 0; sl[i].lr = 0; sl[i].jo = 0; sl[i].w = 0.0f; }
   } else {
@@ -376,14 +403,76 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
     for (int jn = 0; jn < 4; ++jn) {
       const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
-      kaC[jn] = (lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * 0x7feb352dU) ^ zero;
+      const uint32_t ka0 = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
+      kaC[jn] = MODE == 3 ? ka0 : (ka0 * 0x7feb352dU) ^ zero;
     }
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
     const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
     float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // A_j = sum_ik beta_ik c_ikj
-    if (MODE != 0) {
+    if (MODE == 3) {
+      // ---- Zirr & Kaplanyan-style baseline: per LOD of
+      // the pair around the probe area (Eq. 7 output mix, R-33), per probe
+      // along the major axis (R-31/32), 4 bilinear texels x 4 angular nodes,
+      // each an Eq. 15 classical binomial (R-34/35). Variable cost by design.
+      const int32_t ez = (int32_t)((__float_as_uint(zA) >> 23) & 255u) - 127;
+      const int32_t kz = ez >> 1;
+      const float wt = (zA * pow2i(-2 * kz) - 1.0f) * (1.0f / 3.0f);
+      const uint32_t Tp = (uint32_t)ceilf(p * 0x1p24f);
+#pragma unroll 1
+      for (int lev = 0; lev < 2; ++lev) {
+        const int32_t lv = kz + lev;
+        const float wl = lev ? wt : 1.0f - wt;
+        float nt = N * pow2i(2 * lv);
+        if (!(nt <= 0x1p64f)) nt = 0x1p64f;
+        const float np_ = nt * p;
+        const bool gauss = np_ > 5.0f || nt > 16.0f;
+        const float sv = np_ * (1.0f - p);
+        const float sg = sv >= 0x1p-126f ? sv * rsqrt_c(sv) : 0.0f;
+        const float capz = ceilf(nt);
+        const float nf = floorf(nt);
+        const int nfi = gauss ? 0 : (int)nf;
+        const uint32_t Tf = (uint32_t)ceilf(((nt - nf) * p) * 0x1p24f);
+        const float s = pow2i(-lv);
+        const uint32_t lkey = so + (uint32_t)lv * 0x5bd1e995U + 0x68e31da4U;
+#pragma unroll 1
+        for (int k = 0; k < znp; ++k) {
+          const float off = ((float)(2 * k + 1 - znp) * zq) * zsmax;
+          const float uk = __fmaf_rn(off, zex, u), vk = __fmaf_rn(off, zey, v);
+          const float gx = __fmaf_rn(uk, s, -0.5f), gy = __fmaf_rn(vk, s, -0.5f);
+          const float fxs = floorf(gx), fys = floorf(gy);
+          const float fx = gx - fxs, fy = gy - fys;
+          const uint32_t ix = (uint32_t)(long long)fxs, iy = (uint32_t)(long long)fys;
+          const float bq[4] = {(1.0f - fx) * (1.0f - fy), fx * (1.0f - fy), (1.0f - fx) * fy, fx * fy};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t hz = lowbias32(lkey + (ix + (uint32_t)(q & 1)) * 0x8da6b343U +
+                                          (iy + (uint32_t)(q >> 1)) * 0xd8163841U);
+            const float wq = wl * bq[q];
+#pragma unroll
+            for (int jn = 0; jn < 4; ++jn) {
+              const uint32_t w = lowbias32(hz + kaC[jn]);
+              float c;
+              if (gauss) {
+                const float z = sZ[(w >> 2) & (GLINT_ZQ - 1)];
+                float x = __fmaf_rn(sg, z, np_);
+                x = x < 0.0f ? 0.0f : x;
+                x = x > capz ? capz : x;
+                c = floorf(x);
+              } else {
+                int cnt = (lowbias32(w + 16u * 0x9e3779b9U) >> 8) < Tf ? 1 : 0;
+#pragma unroll 1
+                for (int t = 0; t < nfi; ++t) cnt += (lowbias32(w + (uint32_t)t * 0x9e3779b9U) >> 8) < Tp ? 1 : 0;
+                c = (float)cnt;
+              }
+              A[jn] = __fmaf_rn(wq, c, A[jn]);
+            }
+          }
+        }
+      }
+    }
+    if (MODE == 1 || MODE == 2) {
       // ---- ablations: NGA grids x 4 bilinear texels x 4 nodes,
       // everything per light (one grid at a time, rolled: small code)
 #pragma unroll 1
@@ -630,6 +719,7 @@ cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t s
   switch (prm.sc.eval_mode) {
     case 1: return tma ? launch_t<false, true, 1>(prm, grid, stream) : launch_t<false, false, 1>(prm, grid, stream);
     case 2: return tma ? launch_t<false, true, 2>(prm, grid, stream) : launch_t<false, false, 2>(prm, grid, stream);
+    case 3: return tma ? launch_t<false, true, 3>(prm, grid, stream) : launch_t<false, false, 3>(prm, grid, stream);
     default: return tma ? launch_t<false, true, 0>(prm, grid, stream) : launch_t<false, false, 0>(prm, grid, stream);
   }
 }

@@ -219,3 +219,42 @@ def test_ablation_modes(ctx, draws):
         rgb_o, fl_o, _ = oracle.eval(fr.gbuf, fr.scene)
         compare_radiance(out, rgb_o, fl_o, f"{fr.name} draws={draws}")
         assert rgb_o.max() > 0
+
+
+def test_zk_baseline_parity(ctx):
+    """eval_mode 3, the Zirr & Kaplanyan-style baseline:
+    radiance and flags against the oracle on the C1 layouts, C2 crops from
+    grazing (anisotropy beyond the x16 probe cap) to facing, a C3 crop and a
+    random stress buffer with invalid and degenerate pixels."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    cases = [synth.c1("ggx", "mirror"), synth.c1("beckmann", "az90")]
+    for elev, win in ((5, (440, 480, 800, 960)), (25, (400, 464, 800, 1000)), (25, (1016, 1080, 0, 200)),
+                      (90, (500, 532, 0, 256))):
+        cases.append(synth.c2(elev, window=win))
+    cases.append(synth.c3(window=(900, 964, 1700, 1828)))
+    cases.append(synth.Frame("random", synth.random_gbuffer(37, 29, seed=9), synth.random_scene(9, n_lights=3)))
+    for fr in cases:
+        fr.scene.method = "zk"
+        out = pkg.glint_eval(ctx, fr.gbuf.to("cuda"), fr.scene)
+        torch.cuda.synchronize()
+        rgb_o, fl_o, _ = oracle.eval(fr.gbuf, fr.scene)
+        compare_radiance(out, rgb_o, fl_o, f"{fr.name} zk")
+        assert rgb_o.max() > 0
+
+
+def test_zk_full_size_sampled(ctx):
+    """The baseline at full C2 size (25 deg: anisotropic far field) in the
+    bench's launch configuration; sampled pixels recomputed by the oracle."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c2(25, device="cuda")
+    fr.scene.method = "zk"
+    out = pkg.glint_eval(ctx, fr.gbuf, fr.scene).reshape(-1, 4)
+    torch.cuda.synchronize()
+    idx = torch.randint(0, 1920 * 1080, (2000,), generator=torch.Generator().manual_seed(3))
+    sub = fr.gbuf.take(idx).to("cpu")
+    rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+    compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "zk full")
