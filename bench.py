@@ -254,10 +254,12 @@ def run_ours(args):
         with ClockSampler(local) as clk:
             D.barrier()
             torch.cuda.synchronize()
+            torch.cuda.nvtx.range_push("glint_timed")   # ncu --nvtx-include "glint_timed/": the step's launches
             start.record(stream)
             for k in range(args.steps):
                 step(ev_pairs[k])
             end.record(stream)
+            torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
             D.barrier()
         ms = start.elapsed_time(end)

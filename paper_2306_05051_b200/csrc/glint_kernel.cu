@@ -580,15 +580,15 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 
 // ---------------------------------------------------------------------------
 // The kernel: persistent blocks over kTile-pixel tiles, claimed dynamically
-// (the first tile is blockIdx.x, later ones come from this launch's counter:
-// balances per-tile cost variance and the tail). Warp 0 is the producer: one
-// tile ahead of itself it claims the next tile, waits until every warp has
-// released that ring stage, and (TMA: contiguous G-buffer, pitch == width)
-// issues the 5 bulk copies of the tile into it; a full mbarrier per stage
-// carries the tile id and the bytes, an empty mbarrier per stage counts the
-// warps done with it. No block-wide barrier inside the loop: a warp can run
-// up to kStages - 2 tiles ahead of the slowest one. Without TMA the planes
-// are read directly and the ring carries only tile ids.
+// (the first two are blockIdx.x and one claim, later ones come from this
+// launch's counter: balances per-tile cost variance and the tail). Tiles
+// stream through a ring of kStages shared-memory stages; each stage has a
+// full mbarrier (tile id + bytes landed) and a counter of warps done with it.
+// The LAST warp to finish a stage knows it is free: it claims the tile
+// kStages iterations ahead and (TMA: contiguous G-buffer, pitch == width)
+// issues its 5 bulk copies into that stage. No producer warp, no block-wide
+// barrier inside the loop; a warp can run up to kStages - 1 tiles ahead of
+// the slowest one. Without TMA the ring carries only tile ids.
 // ---------------------------------------------------------------------------
 template <bool DEBUG, bool TMA, int MODE>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
@@ -597,10 +597,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* tbar = reinterpret_cast<uint64_t*>(smem);   // tables loaded
   uint64_t* full = tbar + 1;                             // [kStages] tile (and its bytes) ready
-  uint64_t* empty = full + kStages;                      // [kStages] kWarps arrivals: stage free
-  long long* s_tile = reinterpret_cast<long long*>(empty + kStages);   // [kStages] tile ids
+  long long* s_tile = reinterpret_cast<long long*>(full + kStages);   // [kStages] tile ids
+  uint32_t* s_done = reinterpret_cast<uint32_t*>(s_tile + kStages);   // [kStages] warps done
   float4* tiles = reinterpret_cast<float4*>(smem + kSmemTables);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
 
   const glint_scene& sc = prm.sc;
   const int64_t n_pix = (int64_t)prm.width * prm.height;
@@ -610,6 +610,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   const bool flat_out = prm.out_pitch == prm.width;
 
   auto issue = [&](int64_t t, int b) {   // one thread: tile t into stage b (or just its id)
+    s_tile[b] = t;
     if (TMA && t < n_tiles) {
       const int64_t base = t * kTile;
       const int64_t cnt = (n_pix - base) < kTile ? (n_pix - base) : kTile;
@@ -625,36 +626,25 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       mbar_arrive(&full[b]);
     }
   };
+  auto claim = [&]() -> int64_t { return (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull); };
 
   if (tid == 0) {
     mbar_init(tbar, 1);
-    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], kWarps); }
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); s_done[s] = 0u; }
     fence_mbar_init();
     // tables: one bulk copy each (16 KB quantiles, 2 KB orientations)
     mbar_arrive_expect_tx(tbar, (uint32_t)(kSmemZ + kSmemCS));
     bulk_g2s(sZ, prm.ztab, (uint32_t)kSmemZ, tbar);
     bulk_g2s(sCS, prm.cstab, (uint32_t)kSmemCS, tbar);
-    s_tile[0] = blockIdx.x;
+    const bool any = (int64_t)blockIdx.x < n_tiles;
     issue(blockIdx.x, 0);
+    for (int s = 1; s < kStages; ++s) issue(any ? claim() : n_tiles, s);
   }
-  __syncthreads();   // barriers initialised (the only block-wide barrier)
+  __syncthreads();   // barriers initialised
   mbar_wait(tbar, 0u);
 
-  bool more = (int64_t)blockIdx.x < n_tiles;   // producer state (warp 0): claims not yet exhausted
   for (int it = 0;; ++it) {
     const int s = it % kStages;
-    if (warp == 0 && more) {
-      // produce iteration it + 1: its stage was last consumed at it + 1 - kStages
-      const int s1 = (it + 1) % kStages;
-      if (it + 1 >= kStages) mbar_wait(&empty[s1], (uint32_t)((it + 1) / kStages - 1) & 1u);
-      if (lane == 0) {
-        const int64_t nt = (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull);
-        s_tile[s1] = nt;
-        issue(nt, s1);
-        more = nt < n_tiles;
-      }
-      more = __shfl_sync(0xffffffffu, more, 0);
-    }
     mbar_wait(&full[s], (uint32_t)(it / kStages) & 1u);
     const int64_t t = s_tile[s];
     if (t >= n_tiles) break;
@@ -684,10 +674,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
                                nrm, pos, mat, seed_h, inv_beta, prm.zero);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done with stage s
+    if (lane == 0) {
+      // this warp is done with stage s (its reads ordered before the count)
+      __threadfence_block();
+      if (atomicAdd(&s_done[s], 1u) == (uint32_t)(kWarps - 1)) {
+        __threadfence_block();
+        s_done[s] = 0u;
+        issue(claim(), s);   // the tile kStages iterations ahead
+      }
+    }
   }
-  // every block's producer made exactly one failing claim (or none) before
-  // leaving; the last block to finish resets this launch's counters
+  // all claims of this block precede its finish; the last block to finish
+  // resets this launch's counters for the next use of the slot
+  __syncthreads();
   if (tid == 0) {
     __threadfence();
     if (atomicAdd(&prm.sched[1], 1ull) == (unsigned long long)(gridDim.x - 1)) {

@@ -28,8 +28,8 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kSchedSlots = 1024;               // per-context ring of per-launch scheduler counters
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
-constexpr size_t kSmemTables = 256;    // dynamic part: table + 2 x kStages mbarriers, tile ids (padded)
-static_assert(8 * (1 + 2 * kStages) + 8 * kStages <= kSmemTables, "barrier area");
+constexpr size_t kSmemTables = 256;    // dynamic part: table + kStages mbarriers, tile ids, counters (padded)
+static_assert(8 * (1 + kStages) + 8 * kStages + 4 * kStages <= kSmemTables, "barrier area");
 constexpr size_t kSmemTma = kSmemTables + (size_t)kStages * 5 * kTile * 16;  // + kStages x 5 planes x kTile float4
 
 struct KParams {

@@ -13,6 +13,7 @@ if [ "$prof" = "full" ] || [ "$prof" = "both" ]; then
   ncu --set full --clock-control none --import-source on -k regex:glint_eval_kernel -s 3 -c 1 -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_full_$tag.log 2>&1; echo ncu_full_rc=$?
 fi
 if [ "$prof" = "launches" ] || [ "$prof" = "both" ]; then
+  echo "ncu --nvtx --nvtx-include glint_timed/ --metrics gpu__time_duration.sum --clock-control none --csv $CMD" > gpurun_out/launches_$tag.cmd
   $CMD > gpurun_out/plain2_$tag.log 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1; echo ncu_launch_rc=$?
+  ncu --nvtx --nvtx-include "glint_timed/" --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1; echo ncu_launch_rc=$?
 fi

@@ -83,10 +83,16 @@ if launches and os.path.exists(launches):
             if len(r) > vi and r[mi] == "gpu__time_duration.sum":
                 per.setdefault(r[ki].split("(")[0], []).append(float(r[vi].replace(",", "")))
         tot = sum(sum(x) for x in per.values())
-        lines += ["", "Launch list (ncu `--metrics gpu__time_duration.sum`, cold-cache, serialised):", "",
-                  "| kernel | launches | total us | share |", "|---|---|---|---|"]
+        cmdf = launches.replace(".csv", ".cmd")
+        nvtx = os.path.exists(cmdf) and "--nvtx-include" in open(cmdf).read()
+        if os.path.exists(cmdf):
+            lines += ["", "Launch-list command: `" + open(cmdf).read().strip() + "`"]
+        lines += ["", "Launch list (ncu `--metrics gpu__time_duration.sum --clock-control none`, cold-cache, "
+                  "serialised" + (", timed region only: `--nvtx --nvtx-include glint_timed/`" if nvtx else "") + "):", "",
+                  "| kernel | launches | total us | mean us/launch | share |", "|---|---|---|---|---|"]
         for k, x in sorted(per.items(), key=lambda kv: -sum(kv[1])):
-            lines.append(f"| {k} | {len(x)} | {sum(x) / 1e3:.1f} | {100 * sum(x) / tot:.1f}% |")
+            lines.append(f"| {k} | {len(x)} | {sum(x) / 1e3:.1f} | {sum(x) / 1e3 / len(x):.1f} | "
+                         f"{100 * sum(x) / tot:.1f}% |")
         with open(f"profiles/{tag}_launches.csv", "w") as fh:
             fh.write(txt[i:])
 with open(f"profiles/{tag}_ncu.md", "w") as fh:
