@@ -209,6 +209,21 @@ def read_profile_traffic():
     return d.get("dram_bytes_per_launch_per_pixel"), d
 
 
+def measure_h2d_gbs(dev, nbytes=1 << 29, reps=3) -> float:
+    """Best-of-3 pinned host -> device copy bandwidth (GB/s, CUDA events)."""
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    best = 0.0
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        dst.copy_(src, non_blocking=True)
+        b.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+    return best
+
+
 def run_ours(args):
     import paper_2306_05051_b200 as pkg
     from paper_2306_05051_b200 import build as B
@@ -324,6 +339,11 @@ def run_ours(args):
         e2e = {"value": D.sum_over_ranks(evals * n_e2e, device=dev) / t_e2e, "unit": UNIT,
                "h2d_bytes_per_step": int(tot_px * 80), "d2h_bytes_per_step": int(tot_px * 16),
                "steps": n_e2e, "api": "glint_eval_host (pinned host G-buffer -> host radiance)"}
+        # the host link is the e2e bound: compare with a measured pinned H2D copy
+        h2d_peak = measure_h2d_gbs(dev)
+        e2e["h2d_gbs_achieved"] = tot_px * 80 * n_e2e / t_e2e / 1e9
+        e2e["h2d_gbs_measured_peak"] = h2d_peak
+        e2e["h2d_frac"] = e2e["h2d_gbs_achieved"] / h2d_peak
         # sanity: host path reproduces the device path bit for bit
         if not torch.equal(houts[0].view(torch.int32), outs[0].cpu().view(torch.int32)):
             raise SystemExit("glint_eval_host output differs from glint_eval")

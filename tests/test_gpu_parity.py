@@ -258,3 +258,28 @@ def test_zk_full_size_sampled(ctx):
     sub = fr.gbuf.take(idx).to("cpu")
     rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
     compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "zk full")
+
+
+@pytest.mark.parametrize("K,view_kind,beta,ndf", [(1, "point", 0.05, "ggx"), (2, "directional", 0.011, "beckmann"),
+                                                  (5, "point", 0.3, "beckmann"), (8, "directional", 0.05, "ggx")])
+def test_scene_parameter_sweep(ctx, K, view_kind, beta, ndf):
+    """Max ratio level K < 8 (the ratio clamp moves to 2^K, fewer orientation
+    bins), directional views, extreme angular cell sizes, both NDFs: records
+    bit-exact, radiance within 1e-4, all four eval modes' radiance."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    gb = synth.random_gbuffer(41, 53, seed=100 + K)
+    sc = synth.random_scene(100 + K, n_lights=4, ndf=ndf)
+    sc.max_ratio_level, sc.view_kind, sc.beta = K, view_kind, beta
+    if view_kind == "directional":
+        sc.view = (0.2, -0.3, 0.9)
+    (out, rec), (rgb_o, fl_o, rec_o) = run_both(ctx, gb, sc)
+    compare_records(rec, rec_o, f"K{K}")
+    compare_radiance(out, rgb_o, fl_o, f"K{K}")
+    for draws, method in ((64, "ours"), (160, "ours"), (48, "zk")):
+        sc.draws, sc.method = draws, method
+        o = pkg.glint_eval(ctx, gb.to("cuda"), sc)
+        torch.cuda.synchronize()
+        r_o, f_o, _ = oracle.eval(gb, sc)
+        compare_radiance(o, r_o, f_o, f"K{K} {method} {draws}")
