@@ -116,8 +116,23 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- workload
-def make_frames(config: str, device, seed: int):
+C5_FRAMES = 64
+C5_DESC = ("C5: 64-frame 3840x2160 zoom path (distance 0.5 -> 500, elevation 30 deg) over the 32-sphere scene, "
+           "4 point lights, anisotropic GGX alpha U(0.05,0.6), N log-U[1e3,1e7]; frames sharded across ranks, "
+           "radiance gathered to rank 0")
+
+
+def make_frames(config: str, device, seed: int, rank: int = 0, world: int = 1):
     from paper_2306_05051_b200 import synth
+    if config == "C5":
+        # BASELINE.json configs[4]: the zoom path, frames sharded f = rank (mod world);
+        # one fixed image set whatever the GPU count (strong scaling)
+        from paper_2306_05051_b200 import dist as D
+        ids = D.shard(range(C5_FRAMES), rank, world)
+        frames = [synth.c5(f, device=device) for f in ids]
+        for fr, f in zip(frames, ids):
+            fr.frame_id = f
+        return frames, C5_DESC
     if config == "C2":
         frames = synth.c2_frames(device=device)
         desc = ("C2: 1920x1080 infinite ground plane, pinhole 60deg FOV, elevations 5..85 + 90 deg "
@@ -171,11 +186,19 @@ def run_reference(args):
     rank, world, _ = D.env_rank_world()
     if rank != 0:
         return 0
-    frames, desc = make_frames(args.config, "cpu", seed=1)
+    if args.config == "C5":
+        # 64 full 4K frames on the CPU would take minutes to synthesise: the
+        # bounded sample is an 8-row band through the middle of every frame
+        from paper_2306_05051_b200 import synth
+        frames = [synth.c5(f, window=(1076, 1084, 0, 3840)) for f in range(C5_FRAMES)]
+        desc = C5_DESC
+        stride = 1
+    else:
+        frames, desc = make_frames(args.config, "cpu", seed=1)
+        stride = 64 if args.config == "C2" else 256
     for fr in frames:
         fr.scene.draws = args.draws
         fr.scene.method = args.method
-    stride = 64 if args.config == "C2" else 256
     subs = oracle_sample(frames, stride)
     cores = host_cores()
     for _ in range(args.warmup):
@@ -186,11 +209,14 @@ def run_reference(args):
         ev_tot += ev
         t_tot += t
     value = ev_tot / t_tot
-    sample = f"every {stride}th row of each of the {len(frames)} frames of {args.config} ({ev_tot // args.steps} evals/step)"
+    if args.config == "C5":
+        sample = f"rows 1076-1083 of each of the 64 frames of C5 ({ev_tot // args.steps} evals/step)"
+    else:
+        sample = f"every {stride}th row of each of the {len(frames)} frames of {args.config} ({ev_tot // args.steps} evals/step)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
         "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -236,7 +262,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = pkg.Context(local)
-    frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank)
+    frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank, rank=rank, world=world)
     for fr in frames:
         fr.scene.draws = args.draws
         fr.scene.method = args.method
@@ -321,10 +347,30 @@ def run_ours(args):
         roofline["frac_at_measured_clock"] = achieved / (sms * LANES_PER_SM * cs["sm_mhz"] * 1e6)
 
     # ---- end to end through the public C ABI with host buffers
+    # ---- C5: gather every frame's radiance to rank 0 (NCCL p2p), timed apart
+    gather = None
+    if args.config == "C5":
+        D.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        full = D.gather_frames({fr.frame_id: o for fr, o in zip(frames, outs)}, range(C5_FRAMES),
+                               shape=tuple(outs[0].shape), device=dev)
+        torch.cuda.synchronize()
+        t_g = D.max_over_ranks(time.perf_counter() - t0, device=dev)
+        if rank == 0 and sorted(full) != list(range(C5_FRAMES)):
+            raise SystemExit("C5 gather incomplete")
+        gather = {"ms": t_g * 1e3, "frames": C5_FRAMES, "bytes": int(C5_FRAMES * outs[0].numel() * 4),
+                  "how": "torch.distributed send/recv per frame to rank 0, after the timed region"}
+        del full
+
     e2e = None
     if not args.no_e2e:
-        hosts = [fr.gbuf.to("cpu").pin() for fr in frames]
-        houts = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32).pin_memory() for fr in frames]
+        # C5: the first 4 of this rank's frames (pinning 42 GB of host G-buffer is not sensible)
+        sub_n = 4 if args.config == "C5" else len(frames)
+        hosts = [fr.gbuf.to("cpu").pin() for fr in frames[:sub_n]]
+        houts = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32).pin_memory()
+                 for fr in frames[:sub_n]]
+        e_px, _, e_ev = count_evals(frames[:sub_n])
         n_e2e = max(1, min(args.steps, args.e2e_steps))
         for hb, fr, ho in zip(hosts, frames, houts):
             pkg.glint_eval_host(ctx, hb, fr.scene, out=ho)
@@ -336,12 +382,14 @@ def run_ours(args):
                 pkg.glint_eval_host(ctx, hb, fr.scene, out=ho)
         torch.cuda.synchronize()
         t_e2e = D.max_over_ranks(time.perf_counter() - t0, device=dev)
-        e2e = {"value": D.sum_over_ranks(evals * n_e2e, device=dev) / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": int(tot_px * 80), "d2h_bytes_per_step": int(tot_px * 16),
+        e2e = {"value": D.sum_over_ranks(e_ev * n_e2e, device=dev) / t_e2e, "unit": UNIT,
+               "h2d_bytes_per_step": int(e_px * 80), "d2h_bytes_per_step": int(e_px * 16),
                "steps": n_e2e, "api": "glint_eval_host (pinned host G-buffer -> host radiance)"}
+        if sub_n < len(frames):
+            e2e["sample"] = f"first {sub_n} of this rank's {len(frames)} frames"
         # the host link is the e2e bound: compare with a measured pinned H2D copy
         h2d_peak = measure_h2d_gbs(dev)
-        e2e["h2d_gbs_achieved"] = tot_px * 80 * n_e2e / t_e2e / 1e9
+        e2e["h2d_gbs_achieved"] = e_px * 80 * n_e2e / t_e2e / 1e9
         e2e["h2d_gbs_measured_peak"] = h2d_peak
         e2e["h2d_frac"] = e2e["h2d_gbs_achieved"] / h2d_peak
         # sanity: host path reproduces the device path bit for bit
@@ -353,7 +401,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # bounded sample: every 2nd row of the C2 step (~10^7 evals, ~20-30 s of
         # CPU work on 16 cores; ~2 s wall) / every 32nd row of C4
-        stride = 2 if args.config == "C2" else 32
+        stride = 2 if args.config == "C2" else (32 if args.config == "C4" else 256)
         subs = oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride)
         ev, t = time_oracle(subs)
         cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
@@ -364,11 +412,15 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
             "config": {"workload": desc, "pixels_per_step": tot_px, "valid_pixels_per_step": valid_px,
                        "evals_per_step_per_rank": evals, "lights": L, "launches_per_step": len(frames),
-                       "l2": "inputs 1.66 GB per rank > 126 MB L2: no flush between steps",
-                       "parallelism": f"frames x{world} ranks, no data-path collective"},
+                       "l2": f"inputs {tot_px * 80 / 1e9:.2f} GB per rank > 126 MB L2: no flush between steps",
+                       "parallelism": (f"64 frames sharded over {world} ranks (f = rank mod {world}), radiance "
+                                       "gathered to rank 0 after the timed region" if args.config == "C5" else
+                                       f"frames x{world} ranks, no data-path collective"),
+                       **({"gather": gather} if gather else {})},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": cs, "gpu": props.name,
         }
@@ -385,7 +437,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"])
     ap.add_argument("--method", default="ours", choices=["ours", "zk"],
                     help="ours = the paper's method; zk = the Zirr & Kaplanyan-style baseline (eval_mode 3)")
     ap.add_argument("--draws", type=int, default=48, choices=[48, 64, 160],

@@ -283,3 +283,22 @@ def test_scene_parameter_sweep(ctx, K, view_kind, beta, ndf):
         torch.cuda.synchronize()
         r_o, f_o, _ = oracle.eval(gb, sc)
         compare_radiance(o, r_o, f_o, f"K{K} {method} {draws}")
+
+
+@pytest.mark.timeout(300)
+def test_c5_zoom_extremes_sampled(ctx):
+    """C5 (BASELINE configs[4]): the first and last frames of the zoom path
+    (footprint area x10^6 apart, 4 lights) at full 4K, in the bench's launch
+    configuration; sampled pixels recomputed by the oracle."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    for f in (0, 31, 63):
+        fr = synth.c5(f, device="cuda")
+        out = pkg.glint_eval(ctx, fr.gbuf, fr.scene).reshape(-1, 4)
+        torch.cuda.synchronize()
+        idx = torch.randint(0, 3840 * 2160, (800,), generator=torch.Generator().manual_seed(f))
+        sub = fr.gbuf.take(idx).to("cpu")
+        rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+        compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, f"C5 f{f}")
+        del fr, out
