@@ -337,7 +337,10 @@ def run_ours(args):
         "hbm_frac": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9 / float(peaks.get("hbm_gbs", 6458.7)),
         "mean_launch_ms": mean_launch_s * 1e3,
     }
-    if prof and prof.get("sass_thread_inst_per_pixel"):
+    # the committed ncu capture is one C2 frame of the method (48 draws): its
+    # per-pixel SASS count applies to that workload only
+    if prof and prof.get("sass_thread_inst_per_pixel") and args.config == "C2" and args.draws == 48 \
+            and args.method == "ours":
         # issue utilisation from the measured SASS count of the last ncu capture
         roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
         roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
