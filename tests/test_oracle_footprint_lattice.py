@@ -241,3 +241,26 @@ def test_ratio_clamp(orc):
     ls, lr, jo, w, fl = orc.lattice(1.0, 1e6, 0.3)
     assert fl == 4 and max(lr) == 8 and abs(sum(w) - 1) < 1e-6
     assert all(b == 8 for b, wi in zip(lr, w) if wi > 0)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 7])
+def test_lattice_smaller_max_ratio_level(orc, K):
+    """K < 8 (the ABI's max_ratio_level): ratio levels 0..K, orientation
+    indices below 2^lr, partition of unity and area conservation everywhere,
+    the clamp flag exactly when r > 2^K, and any r >= 2^K lattices like r = 2^K
+    (reading R-9; clamp C-25)."""
+    rng = np.random.default_rng(40 + K)
+    for _ in range(4000):
+        P = float(np.float32(2.0 ** rng.uniform(-30, 10)))
+        r = float(np.float32(2.0 ** rng.uniform(0, K + 2)))
+        psi = float(np.float32(rng.random()))
+        ls, lr, jo, w, fl = orc.lattice(P, r, psi, K)
+        w = np.array(w, np.float64)
+        assert w.min() >= -1e-7 and abs(w.sum() - 1) < 2e-6
+        assert abs(sum(wi * 2.0 ** a for wi, a in zip(w, ls)) - P) <= 4e-6 * P
+        for b, c, wi in zip(lr, jo, w):
+            if wi > 0:
+                assert 0 <= b <= K and 0 <= c < 2 ** b
+        assert (fl == 4) == (r > 2.0 ** K)
+        if r >= 2.0 ** K:
+            assert orc.lattice(P, r, psi, K)[:4] == orc.lattice(P, 2.0 ** K, psi, K)[:4]
