@@ -345,6 +345,11 @@ def run_ours(args):
         roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
         roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
         roofline["traffic_source"] = f"profiles/ncu_summary.json ({prof.get('source')})"
+        if prof.get("fp32_flop_per_pixel"):
+            # FP32 arithmetic vs 2 x 128 x SMs x f (not the bound: ALU/issue is)
+            fl = px_per_launch * prof["fp32_flop_per_pixel"] / mean_launch_s
+            roofline["fp32_tflops"] = fl / 1e12
+            roofline["fp32_frac"] = fl / (2 * sms * LANES_PER_SM * f_max)
     cs = clk.summary()
     if cs.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (sms * LANES_PER_SM * cs["sm_mhz"] * 1e6)

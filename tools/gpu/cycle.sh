@@ -10,7 +10,7 @@ cat gpurun_out/bench_$tag.json; tail -3 gpurun_out/bench_$tag.err
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline"
 if [ "$prof" = "full" ] || [ "$prof" = "both" ]; then
   $CMD > gpurun_out/plain_$tag.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:glint_eval_kernel -s 3 -c 1 -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_full_$tag.log 2>&1; echo ncu_full_rc=$?
+  ncu --set full --metrics smsp__sass_thread_inst_executed_op_ffma_pred_on.sum,smsp__sass_thread_inst_executed_op_fadd_pred_on.sum,smsp__sass_thread_inst_executed_op_fmul_pred_on.sum --clock-control none --import-source on -k regex:glint_eval_kernel -s 3 -c 1 -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_full_$tag.log 2>&1; echo ncu_full_rc=$?
 fi
 if [ "$prof" = "launches" ] || [ "$prof" = "both" ]; then
   echo "ncu --nvtx --nvtx-include glint_timed/ --metrics gpu__time_duration.sum --clock-control none --csv $CMD" > gpurun_out/launches_$tag.cmd

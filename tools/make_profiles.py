@@ -59,6 +59,17 @@ summary = {
                          for k in h if k.startswith("smsp__average_warps_issue_stalled_")
                          and k.endswith("_per_issue_active.ratio") and (f(k) or 0) >= 0.05},
 }
+# FP32 arithmetic: FFMA = 2 flops; vs 2 x 128 lanes x SMs x f
+ffma = f("smsp__sass_thread_inst_executed_op_ffma_pred_on.sum")
+fadd = f("smsp__sass_thread_inst_executed_op_fadd_pred_on.sum")
+fmul = f("smsp__sass_thread_inst_executed_op_fmul_pred_on.sum")
+if None not in (ffma, fadd, fmul):
+    flop = 2 * ffma + fadd + fmul
+    sms = f("device__attribute_multiprocessor_count") or 148
+    clk = (summary["sm_clock_ghz"] or 1.965) * 1e9     # ncu reports GHz
+    summary["fp32_flop_per_pixel"] = flop / PIX
+    summary["fp32_tflops"] = flop / (dur_ns * 1e-9) / 1e12
+    summary["fp32_frac_of_peak_at_clock"] = flop / (dur_ns * 1e-9) / (2 * 128 * sms * clk)
 os.makedirs("profiles", exist_ok=True)
 with open("profiles/ncu_summary.json", "w") as fh:
     json.dump(summary, fh, indent=1)
