@@ -336,6 +336,7 @@ def run_ours(args):
         "hbm_achieved_gbs": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9,
         "hbm_frac": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9 / float(peaks.get("hbm_gbs", 6458.7)),
         "mean_launch_ms": mean_launch_s * 1e3,
+        "median_launch_ms": float(np.median(launch_ms)), "min_launch_ms": float(np.min(launch_ms)),
     }
     # the committed ncu capture is one C2 frame of the method (48 draws): its
     # per-pixel SASS count applies to that workload only
