@@ -101,7 +101,8 @@ typedef struct {
  *                                       bit patterns; meta bit0 = pixel valid
  *   nrm = (nx, ny, nz, -)               shading normal (normalised in-kernel)
  *   pos = (x, y, z, -)                  world position (point lights / camera)
- *   mat = (alpha_x, alpha_y, N, R)      roughness, flakes per unit uv^2, glint ratio R
+ *   mat = (alpha_x, alpha_y, N, R)      roughness, flakes per unit uv^2 (clamped to [0, 2^40]; NaN -> 0,
+ *                                       DESIGN.md R-37), glint ratio R (pi ax ay R N P < 2^126 assumed)
  * For glint_eval the planes are device pointers; for glint_eval_host they are
  * host pointers (pinned memory gives full PCIe/C2C bandwidth). */
 typedef struct {

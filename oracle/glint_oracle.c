@@ -729,7 +729,11 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     for (int i = 0; i < 4; ++i) { ls[i] = lr[i] = jo[i] = 0; w[i] = 0.0f; }
   } else if (mode == 2) orc_lattice10(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
   else orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
-  float N = mat[2], R = mat[3], ax = mat[0], ay = mat[1];
+  float R = mat[3], ax = mat[0], ay = mat[1];
+  /* reading R-37: the flake density is clamped to [0, 2^40] (NaN and negative
+   * values to 0), so N 2^ls < 2^104 for every footprint: no overflow */
+  float N = mat[2] > 0.0f ? mat[2] : 0.0f;
+  N = N > 0x1p40f ? 0x1p40f : N;
   for (int i = 0; i < NG; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
 
   /* S3 + S4a: per grid, 3 simplex lattice vertices -- or, in the
@@ -849,7 +853,8 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
 
     /* S8: Eq. 3-4, D_P = D(n)/R * b / N(P), N(P) = N P (reading R-20) */
     double Dn = 1.0 / (M_PI * (double)ax * (double)ay);
-    double Dp = Dn * C / ((double)R * (double)N * (double)P);
+    /* no flake reflects (C = 0, e.g. N = 0 or p = 0): D_P = 0, not 0/0 */
+    double Dp = C > 0.0 ? Dn * C / ((double)R * (double)N * (double)P) : 0.0;
 
     /* S9: Eq. 1-2 with a punctual light: L += F G D_P E / (4 n.wi) */
     double wod[3];

@@ -282,7 +282,10 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     if (MODE == 1)
       for (int i = 0; i < 4; ++i) { als[i] = sl[i].ls; alr[i] = sl[i].lr; ajo[i] = sl[i].jo; aw[i] = sl[i].w; }
   }
-  const float ax = mat.x, ay = mat.y, N = mat.z, R = mat.w;
+  const float ax = mat.x, ay = mat.y, R = mat.w;
+  // flake density clamped to [0, 2^40] (NaN, negative -> 0; R-37): N 2^ls then
+  // stays below 2^104 for every footprint, so trial counts never overflow
+  const float N = fminf(fmaxf(mat.z, 0.0f), 0x1p40f);   // max.f32: NaN -> 0, -0 -> +0
   float n[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) n[i] = sl[i].w * (N * pow2i(sl[i].ls));
@@ -556,7 +559,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       rad_scale = __fdividef(dp_scale, 4.0f * ni);
       have_rad = true;
     }
-    if (DEBUG) { rc->C = C; rc->Dp = C * dp_scale; (void)dhs; }
+    if (DEBUG) { rc->C = C; rc->Dp = C > 0.0f ? C * dp_scale : 0.0f; (void)dhs; }
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
     if (C > 0.0f) {
       const float idl = __fdividef(1.0f, dl);

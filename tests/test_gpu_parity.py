@@ -47,8 +47,12 @@ def compare_records(rg, ro, where=""):
 def compare_radiance(out, rgb_o, fl_o, where=""):
     o = out.reshape(-1, 4).detach().cpu().numpy()
     assert np.array_equal(o[:, 3].view(np.uint32), fl_o), f"{where}: flags"
+    assert np.all(np.isfinite(rgb_o)), f"{where}: oracle radiance not finite"
+    # beyond fp32's range the kernel's correctly rounded answer is +-inf
+    over = np.abs(rgb_o) > np.finfo(np.float32).max
+    assert np.array_equal(o[:, :3][over], np.sign(rgb_o[over]) * np.inf), f"{where}: fp32 overflow"
     err = np.abs(o[:, :3].astype(np.float64) - rgb_o)
-    bad = err > RTOL * np.abs(rgb_o) + 1e-30
+    bad = ~(err <= RTOL * np.abs(rgb_o) + 1e-30) & ~over   # NaN on the GPU side fails too
     assert not bad.any(), (f"{where}: radiance differs at {bad.sum()} values; worst rel "
                            f"{np.max(err / np.maximum(np.abs(rgb_o), 1e-30))}")
 
@@ -333,3 +337,40 @@ def test_concurrent_streams_match_sequential(ctx):
     torch.cuda.synchronize()
     for i, o in enumerate(outs):
         assert torch.equal(o.view(torch.int32), ref[i % len(ref)].view(torch.int32)), i
+
+
+def test_extreme_materials_and_footprints(ctx):
+    """Flake densities 0, tiny, huge and invalid (1e30, 3.4e38, NaN, inf,
+    negative: clamped to [0, 2^40], R-37) over footprints from 2^-60 to 2^60,
+    both paths; records bit-exact, radiance within tolerance."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    H, W = 8, 40
+    g = torch.Generator().manual_seed(11)
+    Ns = torch.tensor([0.0, 1e-30, 1.0, 1e5, 1e20, 1e30, 3.4e38, float("nan"), float("inf"), -1.0, -0.0])
+    Ps = 2.0 ** torch.linspace(-60, 60, W, dtype=torch.float64)
+    duv = torch.zeros(H, W, 4)
+    s = Ps.sqrt().to(torch.float32)
+    duv[..., 0] = s
+    duv[..., 3] = s * 1.7
+    uvm = torch.zeros(H, W, 4)
+    uvm[..., :2] = torch.rand(H, W, 2, generator=g)
+    uvm[..., 2] = synth._bits_to_f32(torch.arange(H * W, dtype=torch.int64).reshape(H, W) * 977)
+    uvm[..., 3] = synth._bits_to_f32(torch.ones(H, W, dtype=torch.int64))
+    nrm = torch.zeros(H, W, 4)
+    nrm[..., 2] = 1.0
+    mat = torch.zeros(H, W, 4)
+    mat[..., 0], mat[..., 1], mat[..., 3] = 0.3, 0.4, 0.5
+    mat[..., 2] = Ns[torch.arange(H * W) % len(Ns)].reshape(H, W)
+    gb = synth.GBuffer(duv, uvm, nrm, torch.zeros(H, W, 4), mat)
+    sc = synth.random_scene(11, n_lights=2)
+    (out, rec), (rgb_o, fl_o, rec_o) = run_both(ctx, gb, sc)
+    compare_records(rec, rec_o, "extreme")
+    compare_radiance(out, rgb_o, fl_o, "extreme")
+    assert np.any((fl_o == 0) & (rgb_o[:, 0] > 0))
+    sc.method = "zk"
+    o = pkg.glint_eval(ctx, gb.to("cuda"), sc)
+    torch.cuda.synchronize()
+    r_o, f_o, _ = oracle.eval(gb, sc)
+    compare_radiance(o, r_o, f_o, "extreme zk")
