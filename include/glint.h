@@ -52,7 +52,7 @@ extern "C" {
 
 /* per-pixel output flags, stored as the bit pattern of out[pixel].w */
 #define GLINT_FLAG_INVALID 1u        /* meta bit0 clear: pixel not shaded */
-#define GLINT_FLAG_DEGENERATE 2u     /* |det J| outside [2^-64, 2^64) or non-finite */
+#define GLINT_FLAG_DEGENERATE 2u     /* |det J| outside [2^-64, 2^64), or major eigenvalue of J J^T >= 2^126 */
 #define GLINT_FLAG_RATIO_CLAMPED 4u  /* anisotropy r > 2^K, clamped (reading R-25) */
 #define GLINT_FLAG_P_CLAMPED 8u      /* R D(h)/D(n) > 1 for some light, clamped (R-19) */
 #define GLINT_FLAG_UV_RANGE 16u      /* |u| or |v| > 2^24 (uv must be tile-local); with INVALID */
@@ -101,8 +101,12 @@ typedef struct {
  *                                       bit patterns; meta bit0 = pixel valid
  *   nrm = (nx, ny, nz, -)               shading normal (normalised in-kernel)
  *   pos = (x, y, z, -)                  world position (point lights / camera)
- *   mat = (alpha_x, alpha_y, N, R)      roughness, flakes per unit uv^2 (clamped to [0, 2^40]; NaN -> 0,
- *                                       DESIGN.md R-37), glint ratio R (pi ax ay R N P < 2^126 assumed)
+ *   mat = (alpha_x, alpha_y, N, R)      roughness, flakes per unit uv^2, glint ratio R; clamped to
+ *                                       alpha in [2^-16, 16], N in [0, 2^40], R in [0, 16], NaN to
+ *                                       the lower bound (R-37). Components of nrm and pos
+ *                                       (and of the scene's view and lights) must satisfy |x| <= 2^60
+ *                                       so that squared lengths stay finite (R-27b); outside that
+ *                                       domain radiance and records are unspecified (no crash)
  * For glint_eval the planes are device pointers; for glint_eval_host they are
  * host pointers (pinned memory gives full PCIe/C2C bandwidth). */
 typedef struct {

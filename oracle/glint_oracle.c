@@ -221,8 +221,9 @@ int orc_footprint(const float duv[4], float* P, float* r, float* psi) {
   float ps = at < 0.0f ? at + 1.0f : at;
   if (ps >= 1.0f) ps = 0.0f;
   *psi = ps;
-  /* reading R-25: valid footprint area is [2^-64, 2^64) */
-  return (*P >= 0x1p-64f && *P < 0x1p64f) ? 1 : 0;
+  /* reading R-25: valid footprint area is [2^-64, 2^64); R-30b: and the
+   * major eigenvalue below 2^126 (so a, c, 2b, a - c are finite) */
+  return (*P >= 0x1p-64f && *P < 0x1p64f && lam < 0x1p126f) ? 1 : 0;
 }
 
 /* ---------------------------------------------------------------------- */
@@ -530,7 +531,7 @@ static void onb_f(const float n[3], float t[3], float bt[3]) {
 static double dot3d(const double a[3], const double b[3]) { return a[0]*b[0] + a[1]*b[1] + a[2]*b[2]; }
 static void normalize3d(double v[3]) { double l = sqrt(dot3d(v, v)); v[0] /= l; v[1] /= l; v[2] /= l; }
 static void onb_d(const double n[3], double t[3], double bt[3]) {
-  double sgn = n[2] >= 0.0 ? 1.0 : -1.0;
+  double sgn = copysign(1.0, n[2]);   /* as onb_f (DESIGN §4.3 S5): -0 gives -1 */
   double a = -1.0 / (sgn + n[2]);
   double b = n[0] * n[1] * a;
   t[0] = 1.0 + sgn * n[0] * n[0] * a; t[1] = sgn * b; t[2] = -sgn * n[0];
@@ -729,11 +730,17 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     for (int i = 0; i < 4; ++i) { ls[i] = lr[i] = jo[i] = 0; w[i] = 0.0f; }
   } else if (mode == 2) orc_lattice10(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
   else orc_lattice(P, r, psi, sc->max_ratio_level, ls, lr, jo, w, &flags);
-  float R = mat[3], ax = mat[0], ay = mat[1];
-  /* reading R-37: the flake density is clamped to [0, 2^40] (NaN and negative
-   * values to 0), so N 2^ls < 2^104 for every footprint: no overflow */
+  /* reading R-37: the material domain -- roughness in [2^-16, 16], flake
+   * density in [0, 2^40], ratio R in [0, 16]; NaN (and -0) go to the lower
+   * bound -- so N 2^ls < 2^104 and pi ax ay R N P < 2^116: no fp32 overflow */
+  float ax = mat[0] >= 0x1p-16f ? mat[0] : 0x1p-16f;
+  ax = ax <= 16.0f ? ax : 16.0f;
+  float ay = mat[1] >= 0x1p-16f ? mat[1] : 0x1p-16f;
+  ay = ay <= 16.0f ? ay : 16.0f;
   float N = mat[2] > 0.0f ? mat[2] : 0.0f;
   N = N > 0x1p40f ? 0x1p40f : N;
+  float R = mat[3] > 0.0f ? mat[3] : 0.0f;
+  R = R <= 16.0f ? R : 16.0f;
   for (int i = 0; i < NG; ++i) n[i] = w[i] * (N * pow2i(ls[i]));
 
   /* S3 + S4a: per grid, 3 simplex lattice vertices -- or, in the
@@ -807,7 +814,9 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     else { d[0] = lt->pos_or_dir[0]; d[1] = lt->pos_or_dir[1]; d[2] = lt->pos_or_dir[2]; }
     float d2 = dot3f(d, d);
     float n_d = dot3f(nf, d);
-    if (!(ni > 0.0f && n_d > 0.0f)) continue; /* light below the horizon: 0 */
+    /* light below the horizon: 0; R-27b: |d|^2 must be a normal float (else
+     * the contract sqrt cannot form |d| and h) */
+    if (!(ni > 0.0f && n_d > 0.0f && d2 >= 0x1p-126f && d2 <= 0x1p120f)) continue;
     if (rc) rc->light_active = 1;
     float dl = d2 * orc_rsqrt(d2);
     float hv[3] = {fmaf(dl, wi[0], d[0]), fmaf(dl, wi[1], d[1]), fmaf(dl, wi[2], d[2])};

@@ -226,7 +226,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const float at = atan2_turns(2.0f * b, a - c);
     psi = at < 0.0f ? at + 1.0f : at;
     if (psi >= 1.0f) psi = 0.0f;
-    if (!(P >= 0x1p-64f && P < 0x1p64f)) {
+    if (!(P >= 0x1p-64f && P < 0x1p64f && lam < 0x1p126f)) {   // R-25, R-30b
       flags = GLINT_FLAG_DEGENERATE;
       ok = false;
     }
@@ -282,10 +282,13 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     if (MODE == 1)
       for (int i = 0; i < 4; ++i) { als[i] = sl[i].ls; alr[i] = sl[i].lr; ajo[i] = sl[i].jo; aw[i] = sl[i].w; }
   }
-  const float ax = mat.x, ay = mat.y, R = mat.w;
-  // flake density clamped to [0, 2^40] (NaN, negative -> 0; R-37): N 2^ls then
-  // stays below 2^104 for every footprint, so trial counts never overflow
-  const float N = fminf(fmaxf(mat.z, 0.0f), 0x1p40f);   // max.f32: NaN -> 0, -0 -> +0
+  // material domain (R-37): roughness in [2^-16, 16], flake density in
+  // [0, 2^40], ratio R in [0, 16]; NaN goes to the lower bound (max.f32 also
+  // maps -0 to +0). Trial counts N 2^ls then stay below 2^104 and the radiance
+  // denominator pi ax ay R N P below 2^116: no fp32 overflow anywhere
+  const float ax = fminf(fmaxf(mat.x, 0x1p-16f), 16.0f), ay = fminf(fmaxf(mat.y, 0x1p-16f), 16.0f);
+  const float N = fminf(fmaxf(mat.z, 0.0f), 0x1p40f);
+  const float R = fminf(fmaxf(mat.w, 0.0f), 16.0f);
   float n[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) n[i] = sl[i].w * (N * pow2i(sl[i].ls));
@@ -370,7 +373,8 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       for (int i = 0; i < 4; ++i) { rc->ls[i] = sl[i].ls; rc->lr[i] = sl[i].lr; rc->jo[i] = sl[i].jo; rc->w[i] = sl[i].w; rc->n[i] = n[i]; }
       for (int q = 0; q < 12; ++q) { rc->lx[q] = (int32_t)dlx[q]; rc->ly[q] = (int32_t)dly[q]; }
     }
-    if (!(ni > 0.0f && nd > 0.0f)) continue;   // light below the horizon (R-27)
+    // light below the horizon (R-27); |d|^2 a normal float (R-27b)
+    if (!(ni > 0.0f && nd > 0.0f && d2 >= 0x1p-126f && d2 <= 0x1p120f)) continue;
     if (DEBUG) rc->light_active = 1u;
     // h = normalize(|d| wi + d)  (proportional to wi + wo, one division less)
     const float dl = d2 * rsqrt_c(d2);

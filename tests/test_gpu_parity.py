@@ -44,7 +44,29 @@ def compare_records(rg, ro, where=""):
         assert np.all(np.abs(a - b) <= RTOL * np.abs(b) + 1e-30), f"{where}: {f}"
 
 
-def compare_radiance(out, rgb_o, fl_o, where=""):
+def well_conditioned(gb, scene, cmin=2.0 ** -7):
+    """Pixels whose shading cosines n.wi, n.wo are >= cmin for every light
+    above the horizon (fp64 from the G-buffer). Below that the fp32 radiance
+    path (cosines of fp32-normalised vectors, relative error ~1e-7 / cos)
+    cannot meet 1e-4 against the fp64 oracle."""
+    def unit(v):
+        return v / np.maximum(np.linalg.norm(v, axis=-1, keepdims=True), 1e-300)
+    nrm = gb.nrm.reshape(-1, 4)[:, :3].cpu().double().numpy()
+    pos = gb.pos.reshape(-1, 4)[:, :3].cpu().double().numpy()
+    n = unit(nrm)
+    wi = unit(np.asarray(scene.view, np.float64) - pos) if scene.view_kind == "point" else unit(
+        np.broadcast_to(np.asarray(scene.view, np.float64), pos.shape))
+    ci = (n * wi).sum(-1)
+    ok = ~((ci > 0) & (ci < cmin))
+    for lt in scene.lights:
+        d = np.asarray(lt.pos_or_dir, np.float64)
+        wo = unit(d - pos) if lt.kind == "point" else unit(np.broadcast_to(d, pos.shape))
+        co = (n * wo).sum(-1)
+        ok &= ~((ci > 0) & (co > 0) & (co < cmin))
+    return ok
+
+
+def compare_radiance(out, rgb_o, fl_o, where="", mask=None):
     o = out.reshape(-1, 4).detach().cpu().numpy()
     assert np.array_equal(o[:, 3].view(np.uint32), fl_o), f"{where}: flags"
     assert np.all(np.isfinite(rgb_o)), f"{where}: oracle radiance not finite"
@@ -53,6 +75,9 @@ def compare_radiance(out, rgb_o, fl_o, where=""):
     assert np.array_equal(o[:, :3][over], np.sign(rgb_o[over]) * np.inf), f"{where}: fp32 overflow"
     err = np.abs(o[:, :3].astype(np.float64) - rgb_o)
     bad = ~(err <= RTOL * np.abs(rgb_o) + 1e-30) & ~over   # NaN on the GPU side fails too
+    if mask is not None:
+        assert np.all(np.isfinite(o[:, :3])), f"{where}: radiance not finite"
+        bad &= mask[:, None]
     assert not bad.any(), (f"{where}: radiance differs at {bad.sum()} values; worst rel "
                            f"{np.max(err / np.maximum(np.abs(rgb_o), 1e-30))}")
 
@@ -374,3 +399,62 @@ def test_extreme_materials_and_footprints(ctx):
     torch.cuda.synchronize()
     r_o, f_o, _ = oracle.eval(gb, sc)
     compare_radiance(o, r_o, f_o, "extreme zk")
+
+
+def _fuzz_gbuffer(h, w, seed, values, geom_values=None):
+    """random_gbuffer with one random component per pixel replaced by one of
+    `values` (u, v only in the uvm plane: obj and meta are bit patterns);
+    nrm and pos draw from `geom_values` if given (their domain, R-27b)."""
+    from paper_2306_05051_b200 import synth
+    gb = synth.random_gbuffer(h, w, seed=seed)
+    rng = np.random.default_rng(seed)
+    planes = [p.clone() for p in gb.planes()]
+    for i in range(h * w):
+        k, c = int(rng.integers(0, 5)), int(rng.integers(0, 4))
+        if k == 1 and c >= 2:
+            c = int(rng.integers(0, 2))
+        vals = geom_values if (geom_values is not None and k in (2, 3)) else values
+        planes[k].view(-1, 4)[i, c] = float(rng.choice(vals))
+    return synth.GBuffer(*planes)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_fuzz_finite_extremes(ctx, seed):
+    """Every pixel has one input component set to +-0, +-subnormal, +-1e38,
+    1e-30 or 3e38 (nrm, pos: up to +-2^60, their domain, R-27b): records
+    bit-exact and radiance within tolerance where the shading cosines are
+    well conditioned."""
+    from paper_2306_05051_b200 import synth
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    gb = _fuzz_gbuffer(32, 48, seed, [0.0, -0.0, 1e-40, -1e-40, 1e38, -1e38, 1e-30, 3.0e38],
+                       [0.0, -0.0, 1e-40, -1e-40, 2.0 ** 60, -(2.0 ** 60), 1e-30, 1e9])
+    sc = synth.random_scene(seed, n_lights=3)
+    mask = well_conditioned(gb, sc)
+    assert mask.mean() > 0.9
+    gd = gb.to("cuda")
+    out, rec = pkg.glint_eval(ctx, gd, sc, debug=True)
+    prod = pkg.glint_eval(ctx, gd, sc)
+    torch.cuda.synchronize()
+    rgb_o, fl_o, rec_o = oracle.eval(gb, sc, debug=True)
+    compare_records(rec, rec_o, f"fuzz{seed}")
+    compare_radiance(prod, rgb_o, fl_o, f"fuzz{seed} production", mask)
+    compare_radiance(out, rgb_o, fl_o, f"fuzz{seed}", mask)
+
+
+def test_fuzz_non_finite_inputs(ctx):
+    """NaN / +-inf in any component (outside the contract's domain except N,
+    R-37, and uv/duv, which are flagged): the kernel neither crashes nor hangs,
+    flags equal the oracle's, and radiance matches wherever the oracle's is
+    finite."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    gb = _fuzz_gbuffer(32, 48, 7, [float("nan"), float("inf"), float("-inf")])
+    sc = synth.random_scene(7, n_lights=3)
+    out = pkg.glint_eval(ctx, gb.to("cuda"), sc).reshape(-1, 4).cpu().numpy()
+    rgb_o, fl_o, _ = oracle.eval(gb, sc)
+    assert np.array_equal(out[:, 3].view(np.uint32), fl_o)
+    fin = np.isfinite(rgb_o).all(1)
+    err = np.abs(out[fin, :3].astype(np.float64) - rgb_o[fin])
+    assert np.all(err <= RTOL * np.abs(rgb_o[fin]) + 1e-30)

@@ -78,3 +78,23 @@ def test_reciprocity_of_the_glint_brdf(orc, ndf):
         # angular weights v_j amplify it by 1/beta (a swapped F or G term would
         # break this by orders of magnitude more)
         assert np.allclose(rgb1 * na, rgb2 * nb, rtol=1e-3, atol=0)
+
+
+def test_negative_zero_normal_frames_agree(orc):
+    """n_z = -0 (a normal in the tangent plane): the fp32 decision frame and
+    the fp64 radiance frame take the same branch of the Duff et al. ONB
+    (sgn = copysign(1, n_z) = -1), so anisotropic G2 matches its fp64 value
+    computed with that frame."""
+    import math
+    from paper_2306_05051_b200 import synth
+    g = dict(duv=np.array([[0.01, 0, 0, 0.01]], np.float32),
+             uvm=np.concatenate([np.array([[0.3, 0.4]], np.float32), np.array([[5]], np.uint32).view(np.float32),
+                                 np.array([[1]], np.uint32).view(np.float32)], 1),
+             nrm=np.array([[0.9, -0.3, -0.0, 0]], np.float32), pos=np.zeros((1, 4), np.float32),
+             mat=np.array([[0.2, 0.7, 1e7, 0.3]], np.float32))
+    sc_n = synth.SceneParams(seed=2, view_kind="directional", view=(0.6, 0.5, 0.3),
+                             lights=[synth.Light("directional", (0.7, -0.1, 0.4), (1, 1, 1))])
+    r_neg = orc.eval(g, sc_n)[0]
+    g["nrm"][0, 2] = np.float32(-1e-30)       # same frame branch (negative), same geometry to fp32
+    r_tiny = orc.eval(g, sc_n)[0]
+    assert r_neg[0, 0] > 0 and abs(r_neg[0, 0] / r_tiny[0, 0] - 1) < 1e-5
