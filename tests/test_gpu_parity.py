@@ -440,6 +440,12 @@ def test_fuzz_finite_extremes(ctx, seed):
     compare_records(rec, rec_o, f"fuzz{seed}")
     compare_radiance(prod, rgb_o, fl_o, f"fuzz{seed} production", mask)
     compare_radiance(out, rgb_o, fl_o, f"fuzz{seed}", mask)
+    for draws, method in ((64, "ours"), (160, "ours"), (48, "zk")):
+        sc.draws, sc.method = draws, method
+        o = pkg.glint_eval(ctx, gd, sc)
+        torch.cuda.synchronize()
+        r_o, f_o, _ = oracle.eval(gb, sc)
+        compare_radiance(o, r_o, f_o, f"fuzz{seed} {method} {draws}", mask)
 
 
 def test_fuzz_non_finite_inputs(ctx):
