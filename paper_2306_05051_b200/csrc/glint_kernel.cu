@@ -575,10 +575,12 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       const float om = 1.0f - cih;
       const float om2 = om * om;
       const float om5 = om2 * om2 * om;
-      const float kk = G2 * C * rad_scale * E;
-      rgb.x += (sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk * lt.intensity[0];
-      rgb.y += (sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk * lt.intensity[1];
-      rgb.z += (sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk * lt.intensity[2];
+      // irradiance I E first: E = 1/d^2 can be ~1e-36 against I ~ 1e36, and
+      // G2 C rad_scale E alone would go subnormal (lost bits)
+      const float kk = G2 * C * rad_scale;
+      rgb.x += (sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk * (lt.intensity[0] * E);
+      rgb.y += (sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk * (lt.intensity[1] * E);
+      rgb.z += (sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk * (lt.intensity[2] * E);
     }
   }
   if (DEBUG) for (int l = 0; l < L; ++l) rec[l].flags = flags;
