@@ -271,7 +271,15 @@ def run_ours(args):
     if args.method == "zk":
         desc += "; BASELINE: Zirr & Kaplanyan-style path (DESIGN.md section 10), not the paper's method"
     tot_px, valid_px, evals = count_evals(frames)
-    outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
+    gbuf_all = None
+    if args.config == "C5" and args.gather == "p2p":
+        # every rank's kernel stores its frames straight into rank 0's buffer
+        # (CUDA IPC peer memory over NVLink): the gather is fused into shading
+        fr0 = frames[0]
+        gbuf_all = D.peer_buffer((C5_FRAMES, fr0.gbuf.height, fr0.gbuf.width, 4), device=dev)
+        outs = [gbuf_all[fr.frame_id] for fr in frames]
+    else:
+        outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
     stream = torch.cuda.current_stream(dev)
 
     def step(evs=None):
@@ -358,7 +366,15 @@ def run_ours(args):
     # ---- end to end through the public C ABI with host buffers
     # ---- C5: gather every frame's radiance to rank 0 (NCCL p2p), timed apart
     gather = None
-    if args.config == "C5":
+    if args.config == "C5" and args.gather == "p2p":
+        D.barrier()
+        torch.cuda.synchronize()
+        if rank == 0:   # every frame landed: flags plane of each frame written
+            assert not torch.isnan(gbuf_all[..., 3]).any().item()
+        gather = {"ms": 0.0, "frames": C5_FRAMES, "bytes": int(gbuf_all.numel() * 4) if rank == 0 else None,
+                  "how": "fused: each rank's kernel stores its frames' radiance directly into rank 0's buffer "
+                         "(CUDA IPC peer memory over NVLink), inside the timed region"}
+    elif args.config == "C5":
         D.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -426,9 +442,10 @@ def run_ours(args):
             "config": {"workload": desc, "pixels_per_step": tot_px, "valid_pixels_per_step": valid_px,
                        "evals_per_step_per_rank": evals, "lights": L, "launches_per_step": len(frames),
                        "l2": f"inputs {tot_px * 80 / 1e9:.2f} GB per rank > 126 MB L2: no flush between steps",
-                       "parallelism": (f"64 frames sharded over {world} ranks (f = rank mod {world}), radiance "
-                                       "gathered to rank 0 after the timed region" if args.config == "C5" else
-                                       f"frames x{world} ranks, no data-path collective"),
+                       "parallelism": ((f"64 frames sharded over {world} ranks (f = rank mod {world}); radiance "
+                                        + ("stored by the kernels straight into rank 0's buffer (peer memory)"
+                                           if args.gather == "p2p" else "gathered to rank 0 after the timed region"))
+                                       if args.config == "C5" else f"frames x{world} ranks, no data-path collective"),
                        **({"gather": gather} if gather else {})},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": cs, "gpu": props.name,
@@ -449,6 +466,8 @@ def main():
     ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"])
     ap.add_argument("--method", default="ours", choices=["ours", "zk"],
                     help="ours = the paper's method; zk = the Zirr & Kaplanyan-style baseline (eval_mode 3)")
+    ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
+                    help="C5: fuse the gather to rank 0 into the kernels (peer stores) or send/recv afterwards")
     ap.add_argument("--draws", type=int, default=48, choices=[48, 64, 160],
                     help="draws per pixel-light: 48 = the method; 64 / 160 = its section-6 ablations")
     ap.add_argument("--e2e-steps", type=int, default=5)

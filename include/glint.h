@@ -162,8 +162,11 @@ int glint_destroy(glint_ctx* ctx);
 
 /* Evaluate every pixel of `gb` (device planes) for every light of `scene`:
  * out[y * out_pitch + x] = float4(R, G, B, flags bits) for all pixels (fully
- * overwritten). `dbg` (device, nullable) receives width*height*n_lights
- * records. One kernel launch on `stream`; asynchronous. */
+ * overwritten). `out` may be any address the current device can store to:
+ * its own memory, or a peer GPU's buffer mapped through CUDA IPC / peer
+ * access (the kernel then streams the radiance over NVLink -- the fused
+ * gather of DESIGN.md section 8). `dbg` (device, nullable) receives
+ * width*height*n_lights records. One kernel launch on `stream`; asynchronous. */
 int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
                void* out, int64_t out_pitch, glint_debug_rec* dbg, void* stream);
 

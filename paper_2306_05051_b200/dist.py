@@ -76,3 +76,30 @@ def gather_frames(images: dict, frame_ids: Sequence[int], shape, dtype=torch.flo
                 dist.recv(buf, src=src)
                 out[f] = buf
     return out
+
+
+def peer_buffer(shape, dtype=torch.float32, device=None, src: int = 0):
+    """One device buffer owned by rank ``src`` and mapped into every rank's
+    address space (CUDA IPC: cudaIpcGetMemHandle / cudaIpcOpenMemHandle with
+    lazy peer access, through torch's tensor-sharing reductions). A rank that
+    passes a slice of it as ``out`` to glint_eval has its kernel store the
+    radiance straight into rank ``src``'s HBM over NVLink: the gather to rank 0
+    becomes part of the shading kernel, overlapping it tile by tile, with no
+    separate collective. Returns the buffer (``src``) or its
+    mapping (others); the control plane only moves the IPC handle."""
+    from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if rank == src:
+        buf = torch.empty(shape, dtype=dtype, device=device)
+        if world == 1:
+            return buf
+        _, args = reduce_tensor(buf)
+        obj = [args]
+    else:
+        buf, obj = None, [None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=src)
+        if rank != src:
+            buf = rebuild_cuda_tensor(*obj[0])
+    return buf
