@@ -173,8 +173,9 @@ int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene*
 /* End-to-end entry with HOST buffers: copies the planes host->device, runs the
  * kernel and copies the radiance device->host, pipelined over row chunks on
  * two internal streams (copy/compute overlap). Uses device staging owned by
- * the context (grown on demand, freed by glint_destroy); NOT reentrant on one
- * context. Synchronous: returns after `out` (host, out_pitch float4 per row)
+ * the context (grown on demand, freed by glint_destroy); concurrent calls on
+ * one context are serialised by an internal lock (use one context per thread
+ * for parallel host pipelines). Synchronous: returns after `out` (host, out_pitch float4 per row)
  * is complete. `stream` orders the work after the caller's prior work. */
 int glint_eval_host(glint_ctx* ctx, const glint_gbuffer* gb_host, const glint_scene* scene,
                     void* out_host, int64_t out_pitch, void* stream);

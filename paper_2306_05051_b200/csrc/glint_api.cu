@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "../../include/glint.h"
 #include "glint_kernel.h"
@@ -42,6 +43,7 @@ struct glint_ctx {
   float4* d_stage[2][6];
   cudaStream_t st[2];
   cudaEvent_t ev_in, ev_done[2];
+  std::mutex host_mu;   // serialises glint_eval_host (staging and streams are per context)
 };
 
 extern "C" int glint_version(void) { return GLINT_VERSION; }
@@ -312,6 +314,7 @@ extern "C" int glint_eval_host(glint_ctx* c, const glint_gbuffer* gb, const glin
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
+  std::lock_guard<std::mutex> lock(c->host_mu);
   const int W = gb->width, H = gb->height;
   // ~1M pixels per chunk (80 MB in, 16 MB out), at least 1 row
   int rows = (int)((1 << 20) / W);

@@ -502,3 +502,27 @@ def test_fuzz_scene_parameters(ctx, seed):
     compare_records(rec, rec_o, f"scene fuzz {seed}")
     compare_radiance(prod, rgb_o, fl_o, f"scene fuzz {seed} production", mask)
     compare_radiance(out, rgb_o, fl_o, f"scene fuzz {seed}", mask)
+
+
+def test_host_entry_concurrent_threads(ctx):
+    """glint_eval_host from 3 threads on one context: the internal lock
+    serialises the staging; every output equals the device entry's."""
+    import threading
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    frames = [synth.c2(e, window=(300, 812, 0, 1920)) for e in (20, 45, 70)]
+    refs = [pkg.glint_eval(ctx, fr.gbuf.to("cuda"), fr.scene).cpu() for fr in frames]
+    hosts = [fr.gbuf.pin() for fr in frames]
+    outs = [None] * 3
+
+    def work(i):
+        for _ in range(3):
+            outs[i] = pkg.glint_eval_host(ctx, hosts[i], frames[i].scene)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for o, r in zip(outs, refs):
+        assert torch.equal(o.view(torch.int32), r.view(torch.int32))
