@@ -166,7 +166,11 @@ int glint_destroy(glint_ctx* ctx);
  * its own memory, or a peer GPU's buffer mapped through CUDA IPC / peer
  * access (the kernel then streams the radiance over NVLink -- the fused
  * gather of DESIGN.md section 8). `dbg` (device, nullable) receives
- * width*height*n_lights records. One kernel launch on `stream`; asynchronous. */
+ * width*height*n_lights records. One kernel launch on `stream`; asynchronous;
+ * no host synchronisation or allocation, so it can be captured in a CUDA
+ * graph. Each launch owns one slot of a ring of 1024 tile-scheduler counters
+ * (reset by the launch itself): a captured launch keeps its slot, so one graph
+ * must not be replayed concurrently with itself. */
 int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
                void* out, int64_t out_pitch, glint_debug_rec* dbg, void* stream);
 

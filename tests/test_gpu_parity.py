@@ -526,3 +526,34 @@ def test_host_entry_concurrent_threads(ctx):
         t.join()
     for o, r in zip(outs, refs):
         assert torch.equal(o.view(torch.int32), r.view(torch.int32))
+
+
+def test_cuda_graph_capture_and_replay(ctx):
+    """A step of several glint_eval launches captured into a CUDA graph and
+    replayed: each launch resets its scheduler slot at exit, so replays are
+    bit-identical to eager launches (graph-friendly: no host sync, no
+    allocation inside glint_eval)."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    frames = [synth.c2(e, window=(300, 556, 0, 1920), device="cuda") for e in (25, 65)]
+    outs = [torch.empty(256, 1920, 4, device="cuda") for _ in frames]
+    refs = [pkg.glint_eval(ctx, fr.gbuf, fr.scene).clone() for fr in frames]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):          # warm-up on the capture stream
+        for fr, o in zip(frames, outs):
+            pkg.glint_eval(ctx, fr.gbuf, fr.scene, out=o, stream=s)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st = torch.cuda.current_stream()
+        for fr, o in zip(frames, outs):
+            pkg.glint_eval(ctx, fr.gbuf, fr.scene, out=o, stream=st)
+    for _ in range(3):
+        for o in outs:
+            o.fill_(float("nan"))
+        g.replay()
+        torch.cuda.synchronize()
+        for o, r in zip(outs, refs):
+            assert torch.equal(o.view(torch.int32), r.view(torch.int32))
