@@ -565,7 +565,9 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     }
     if (DEBUG) { rc->C = C; rc->Dp = C > 0.0f ? C * dp_scale : 0.0f; (void)dhs; }
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
-    if (C > 0.0f) {
+    // warp-uniform: lanes with C = 0 add exactly 0 (their D_P term is 0), so
+    // the radiance block runs without per-lane divergence
+    if (DEBUG ? (C > 0.0f) : __any_sync(am, C > 0.0f)) {
       const float idl = __fdividef(1.0f, dl);
       const float wox = dx * idl, woy = dy * idl, woz = dz * idl;
       const float E = (lt.kind == 0) ? __fdividef(1.0f, d2) : 1.0f;
