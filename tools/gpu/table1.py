@@ -92,6 +92,24 @@ def main():
         for method in ("ours", "zk"):
             ts = [r["ms"] for r in rows if r["scene"] == name and r["method"] == method]
             lines.append(f"| {name} | {method} | " + " | ".join(f"{t:.3f}" for t in ts) + " |")
+    # the C2 workload itself per elevation (GGX alpha 0.2, per-tile density 2^U(8,20)):
+    # stable cost vs anisotropy
+    lines += ["", "C2 workload per elevation (ms per 1920x1080 frame; valid-pixel evals/s):", "",
+              "| elevation | valid px | ours ms | ours evals/s | zk ms | zk evals/s | zk / ours |", "|---|---|---|---|---|---|---|"]
+    elev_rows = []
+    for e in synth.C2_ELEVATIONS:
+        fr = synth.c2(e, device=dev)
+        valid = fr.gbuf.valid_count()
+        res = {}
+        for method in ("ours", "zk"):
+            fr.scene.method = method
+            res[method] = time_frame(ctx, fr.gbuf, fr.scene, a.reps)
+        elev_rows.append(dict(elev=e, valid=valid, **{f"{k}_ms": v for k, v in res.items()}))
+        lines.append(f"| {e:g} | {valid} | {res['ours']:.3f} | {valid / res['ours'] / 1e-3:.3e} | {res['zk']:.3f} | "
+                     f"{valid / res['zk'] / 1e-3:.3e} | {res['zk'] / res['ours']:.2f} |")
+    with open(a.out + ".json", "w") as f:
+        json.dump(dict(densities=DENSITIES, rows=rows, c2_elevations=elev_rows, device=torch.cuda.get_device_name(0)), f,
+                  indent=1)
     with open(a.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
