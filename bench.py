@@ -432,6 +432,11 @@ def run_ours(args):
         cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
                "sample": f"every {stride}th row of each of the {len(frames)} frames ({ev} evals, {t:.1f} s wall, "
                          f"{t * host_cores():.0f} core-s)"}
+        # the single-core figure beside the all-core one (a 16x sparser row sample)
+        ev1, t1 = time_oracle(oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride * 16),
+                              threads=1)
+        cpu["value_1core"] = ev1 / t1
+        cpu["sample_1core"] = f"every {stride * 16}th row, 1 thread ({ev1} evals, {t1:.1f} s)"
 
     if rank == 0:
         line = {
