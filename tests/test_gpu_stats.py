@@ -140,3 +140,31 @@ def test_expectation_at_scale(ctx):
         m = stats.pmf_mean(pmf)
         se = math.sqrt(float(np.dot((np.arange(len(pmf)) - m) ** 2, pmf)) / len(c)) * 2.0  # draws share seeds
         assert abs(c.mean() - m) < 4 * se + 1e-12, (i, ni, c.mean(), m, se)
+
+
+def test_convergence_to_smooth_ndf_on_device(ctx):
+    """North-star check 3 on the device (Eq. 5-6): over 256^2 independent
+    surface points, D_P / D(h) has mean -> 1 and a spread that shrinks about
+    sqrt(10)-fold per decade of N P (tools/gpu/convergence.py at full scale)."""
+    import importlib.util
+    import os
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    spec = importlib.util.spec_from_file_location(
+        "convergence", os.path.join(os.path.dirname(__file__), "..", "tools", "gpu", "convergence.py"))
+    cv = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(cv)
+    dev = torch.device("cuda", 0)
+    n, P = 256, 2.0 ** -10
+    t, e = math.radians(20.0), math.radians(5.0)
+    sc = synth.SceneParams(seed=3, ndf="ggx", view_kind="directional", view=(math.sin(t + e), 0.0, math.cos(t + e)),
+                           lights=[synth.Light("directional", (math.sin(t - e), 0.0, math.cos(t - e)), (1.0, 1.0, 1.0))])
+    ref = pkg.glint_eval(ctx, cv.quad(n, P, 2.0 ** 40, 0.35, dev), sc)[..., 0].double().mean().item()
+    spreads = []
+    for NP in (1e3, 1e4, 1e5, 1e6):
+        L = pkg.glint_eval(ctx, cv.quad(n, P, NP / P, 0.35, dev), sc)[..., 0].double() / ref
+        spreads.append(float(L.std()))
+        if NP >= 1e5:
+            assert abs(float(L.mean()) - 1) < 0.01
+    for a, b in zip(spreads, spreads[1:]):
+        assert 2.3 < a / b < 4.3, spreads
