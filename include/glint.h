@@ -158,7 +158,7 @@ int glint_build_tables(float* z, float* cosv, float* sinv);
  * after creation; glint_eval may be called concurrently on different streams.
  * Returns GLINT_EDEVICE if no sm_100 device is present. */
 int glint_create(glint_ctx** out, int device);
-int glint_destroy(glint_ctx* ctx);
+int glint_destroy(glint_ctx* ctx);   /* waits for the device (cudaDeviceSynchronize), then frees */
 
 /* Evaluate every pixel of `gb` (device planes) for every light of `scene`:
  * out[y * out_pitch + x] = float4(R, G, B, flags bits) for all pixels (fully

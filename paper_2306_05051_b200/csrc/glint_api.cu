@@ -158,6 +158,9 @@ extern "C" int glint_destroy(glint_ctx* c) {
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
+  // launches still in flight on callers' streams read the tables and the
+  // scheduler counters freed below: wait for the device first
+  cudaDeviceSynchronize();
   free_stage(c);
   for (int b = 0; b < 2; ++b) {
     if (c->st[b]) cudaStreamDestroy(c->st[b]);
