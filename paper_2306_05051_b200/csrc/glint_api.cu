@@ -246,7 +246,8 @@ static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, c
   k.height = gb->height;
   k.pitch = gb->pitch;
   k.out_pitch = out_pitch;
-  k.zero = 0u;
+  k.c1s = 0x7feb352du;   // the draw hash's first multiplier, twice (see KParams)
+  k.c1n = 0x7feb352du;
   k.sched = c->d_sched + 2 * slot;
   k.sc = *sc;
   return k;

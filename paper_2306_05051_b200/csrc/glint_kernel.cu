@@ -197,7 +197,7 @@ template <bool DEBUG, int MODE>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
-                                            uint32_t seed_h, float inv_beta, uint32_t zero) {
+                                            uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n) {
   const int L = sc.n_lights;
   uint32_t flags = 0;
   const uint32_t meta = __float_as_uint(uvm.w);
@@ -324,9 +324,9 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const uint32_t lin1 = base + (lower ? 0x8da6b343U : 0xd8163841U);
     const uint32_t lin2 = base + (0x8da6b343U + 0xd8163841U);
     const uint32_t h0 = lowbias32(base), h1 = lowbias32(lin1), h2 = lowbias32(lin2);
-    hsC[i * 3 + 0] = (h0 * 0x7feb352dU) ^ zero;
-    hsC[i * 3 + 1] = (h1 * 0x7feb352dU) ^ zero;
-    hsC[i * 3 + 2] = (h2 * 0x7feb352dU) ^ zero;
+    hsC[i * 3 + 0] = h0 * c1s;
+    hsC[i * 3 + 1] = h1 * c1s;
+    hsC[i * 3 + 2] = h2 * c1s;
     if (DEBUG) {
       dlx[i * 3 + 0] = ix; dly[i * 3 + 0] = iy;
       dlx[i * 3 + 1] = lower ? ix + 1u : ix; dly[i * 3 + 1] = lower ? iy : iy + 1u;
@@ -411,7 +411,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     for (int jn = 0; jn < 4; ++jn) {
       const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
       const uint32_t ka0 = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
-      kaC[jn] = MODE == 3 ? ka0 : (ka0 * 0x7feb352dU) ^ zero;
+      kaC[jn] = MODE == 3 ? ka0 : ka0 * c1n;
     }
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
@@ -503,7 +503,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         const uint32_t lin[4] = {base, base + 0x8da6b343U, base + 0xd8163841U, base + (0x8da6b343U + 0xd8163841U)};
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t hC = (lowbias32(lin[k]) * 0x7feb352dU) ^ zero;
+          const uint32_t hC = lowbias32(lin[k]) * c1s;
 #pragma unroll
           for (int jn = 0; jn < 4; ++jn) {
             uint32_t y = hC + kaC[jn];
@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
         oi = (int64_t)y * prm.out_pitch + x;
       }
       shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
-                               nrm, pos, mat, seed_h, inv_beta, prm.zero);
+                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n);
     }
     __syncwarp();
     if (lane == 0) {

@@ -46,8 +46,9 @@ struct KParams {
   int64_t pitch, out_pitch;
   unsigned long long* sched;  // [tile counter, finished blocks] of this launch (dynamic tiles);
                               // zero on entry, reset to zero by the last block
-  uint32_t zero;        // always 0; XOR-ing pre-multiplied seeds with it stops ptxas
-                        // from re-factoring hs*C1 + ka*C1 into (hs + ka)*C1 per draw
+  uint32_t c1s, c1n;    // both 0x7feb352d (the draw hash's first multiplier), passed
+                        // as two runtime values so that ptxas cannot prove them
+                        // equal and re-factor hs*C1 + ka*C1 into (hs + ka)*C1 per draw
   glint_scene sc;
 };
 
