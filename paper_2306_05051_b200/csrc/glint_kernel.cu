@@ -21,6 +21,16 @@
 #include "glint_kernel.h"
 #include "glint_tma.cuh"
 
+// -DGLINT_CHECKED: device asserts on every computed index (compute-sanitizer
+// is not available on this pool); tests/test_gpu_checked.py runs the parity
+// suite's inputs against a checked build
+#ifdef GLINT_CHECKED
+#include <cassert>
+#define GL_ASSERT(c) assert(c)
+#else
+#define GL_ASSERT(c) ((void)0)
+#endif
+
 namespace glint {
 
 // ---------------------------------------------------------------------------
@@ -302,6 +312,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   uint32_t dlx[DEBUG ? 12 : 1], dly[DEBUG ? 12 : 1], dhs[DEBUG ? 12 : 1];
 #pragma unroll
   for (int i = 0; i < (MODE == 0 ? 4 : 0); ++i) {
+    GL_ASSERT(sl[i].lr >= 0 && sl[i].lr <= 8 && sl[i].jo >= 0 && (sl[i].jo >> sl[i].lr) == 0);
     const float2 cs = sCS[sl[i].jo << (8 - sl[i].lr)];
     const float xr = __fmaf_rn(cs.x, u, cs.y * v);
     const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
@@ -488,6 +499,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         const Gate gt = gate_params(ng, p, L2);
         const uint32_t G = (gt.T << 9) - 1u;
         const float capk = gt.T ? gt.cap : 0.0f;
+        GL_ASSERT(alr[g] >= 0 && alr[g] <= 8 && ajo[g] >= 0 && (ajo[g] >> alr[g]) == 0);
         const float2 cs = sCS[ajo[g] << (8 - alr[g])];
         const float xr = __fmaf_rn(cs.x, u, cs.y * v);
         const float yr = __fmaf_rn(cs.x, v, -(cs.y * u));
@@ -625,6 +637,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
     if (TMA && t < n_tiles) {
       const int64_t base = t * kTile;
       const int64_t cnt = (n_pix - base) < kTile ? (n_pix - base) : kTile;
+      GL_ASSERT(t >= 0 && base < n_pix && cnt > 0 && b >= 0 && b < kStages);
       const uint32_t bytes = (uint32_t)cnt * 16u;
       fence_proxy_async_smem();
       mbar_arrive_expect_tx(&full[b], 5u * bytes);
@@ -681,6 +694,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
         pos = __ldcs(prm.pos + gi); mat = __ldcs(prm.mat + gi);
         oi = (int64_t)y * prm.out_pitch + x;
       }
+      GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
+                oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
       shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
                                nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n);
     }
