@@ -557,3 +557,19 @@ def test_cuda_graph_capture_and_replay(ctx):
         torch.cuda.synchronize()
         for o, r in zip(outs, refs):
             assert torch.equal(o.view(torch.int32), r.view(torch.int32))
+
+
+def test_host_entry_pitched_views(ctx):
+    """glint_eval_host on row-pitched host views (a 700-wide window of 1920-wide
+    pinned planes, 1500 rows: a partial last chunk) equals the device entry on
+    the same window."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c2(40, width=1920, height=1500)
+    host = fr.gbuf.pin()
+    view = synth.GBuffer(*[p[:, 600:1300] for p in host.planes()])
+    out_h = pkg.glint_eval_host(ctx, view, fr.scene)
+    dev_view = synth.GBuffer(*[p[:, 600:1300].contiguous() for p in fr.gbuf.to("cuda").planes()])
+    out_d = pkg.glint_eval(ctx, dev_view, fr.scene)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h.view(torch.int32), out_d.cpu().view(torch.int32))
