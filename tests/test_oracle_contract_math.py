@@ -193,3 +193,32 @@ def test_angular_node_draws_are_nearly_uncorrelated(orc):
             for b in range(a + 1, 4):
                 assert abs(np.corrcoef(g[a], g[b])[0, 1]) < 0.02
                 assert abs(np.corrcoef(q[a], q[b])[0, 1]) < 0.02
+
+
+def test_contract_constants_are_the_fp32_closed_forms():
+    """Every polynomial coefficient in the oracle's contract functions is the
+    fp32 rounding of its closed form: ln2^i/i! (exp2),
+    1/(2i+1) (atanh series), (-1)^i/((2i+1) 2 pi) (atan in turns), plus
+    tan(pi/8), 2/ln2 and log2(e). Read from the source text, recomputed here."""
+    import math
+    import os
+    import re
+    src = open(os.path.join(os.path.dirname(__file__), "..", "oracle", "glint_oracle.c")).read()
+
+    def lits(fn):
+        body = src[src.index(fn):]
+        body = body[:body.index("\n}\n")]
+        return [float.fromhex(x) * (-1 if s else 1)
+                for s, x in re.findall(r"(-?)\s*(0x1\.[0-9a-f]+p[-+]?\d+)f", body)]
+
+    f32 = lambda x: float(np.float32(x))
+    exp2 = lits("float orc_exp2(")
+    assert exp2[:7] == [f32(math.log(2) ** i / math.factorial(i)) for i in range(7, 0, -1)]
+    ath = lits("static float atanh_series(")
+    assert ath == [f32(1.0 / (2 * i + 1)) for i in range(7, 0, -1)]
+    at = lits("float orc_atan2_turns(")
+    assert at[0] == f32(math.tan(math.pi / 8))
+    assert at[1:] == [f32((-1) ** i / ((2 * i + 1) * 2 * math.pi)) for i in range(8, -1, -1)]
+    assert float.fromhex("0x1.715476p+1") == f32(2 / math.log(2))
+    assert float.fromhex("0x1.715476p+0") == f32(1 / math.log(2))
+    assert "0x1.715476p+1f" in src
