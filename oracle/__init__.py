@@ -120,6 +120,8 @@ def lib():
             L.orc_zk_lod.restype = None
             L.orc_zk_count.argtypes = [C.c_uint32, C.c_float, C.c_float]
             L.orc_zk_count.restype = C.c_float
+            L.orc_contract_checksum.argtypes = [C.c_int32, C.c_uint64, C.c_uint64]
+            L.orc_contract_checksum.restype = C.c_uint64
             L.orc_init()
             _lib = L
     return _lib
@@ -320,3 +322,14 @@ def zk_lod(A: float):
 
 def zk_count(w: int, nt: float, p: float) -> int:
     return int(lib().orc_zk_count(w & 0xFFFFFFFF, nt, p))
+
+
+def contract_checksum(fn: int, lo: int, hi: int, threads: int | None = None) -> int:
+    """orc_contract_checksum over [lo, hi), split over host threads (the sum is
+    order-independent, mod 2^64)."""
+    threads = threads or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else 1)
+    step = max(1, (hi - lo + 4 * threads - 1) // (4 * threads))
+    parts = [(a, min(hi, a + step)) for a in range(lo, hi, step)]
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        sums = list(ex.map(lambda r: lib().orc_contract_checksum(fn, r[0], r[1]), parts))
+    return sum(sums) % (1 << 64)

@@ -907,3 +907,43 @@ int orc_eval(const float* duv, const float* uvm, const float* nrm, const float* 
                rgb + 3 * i, flags + i, rec ? rec + i * sc->n_lights : 0);
   return 0;
 }
+
+
+/* ---------------------------------------------------------------------- */
+/* Exhaustive contract-math checksums (SURVEY 8c-2 "Contract math itself"):
+ * an order-independent 64-bit sum over an input range of
+ * bits(f(x)) * (index * golden | 1), NaN results canonicalised (payload bits
+ * differ between CPU and GPU). The GPU test library computes the same sum
+ * with the product's device functions; equal sums over all 2^32 inputs mean
+ * bit-equal functions. fn: 0 exp2 (y <= 0 or NaN), 1 log2(1-p) (0 < p < 1),
+ * 2 rcp (normal x > 0), 3 rsqrt (normal x > 0), 4 atan2 in turns on hashed
+ * finite pairs, 5 lowbias32 (all inputs). Test infrastructure.            */
+/* ---------------------------------------------------------------------- */
+static uint64_t cs_term(uint64_t idx, uint32_t bits) {
+  return (uint64_t)bits * ((idx * 0x9E3779B97F4A7C15ull) | 1ull);
+}
+static uint32_t cs_bits(float r) { return r != r ? 0x7FC00000u : f2u(r); }
+
+uint64_t orc_contract_checksum(int32_t fn, uint64_t lo, uint64_t hi) {
+  orc_init();
+  uint64_t acc = 0;
+  for (uint64_t i = lo; i < hi; ++i) {
+    uint32_t b = (uint32_t)i;
+    float x = u2f(b);
+    switch (fn) {
+      case 0: if (!(x > 0.0f)) acc += cs_term(i, cs_bits(orc_exp2(x))); break;
+      case 1: if (x > 0.0f && x < 1.0f) acc += cs_term(i, cs_bits(orc_log2_1mp(x))); break;
+      case 2: if (x >= 0x1p-126f && x <= 0x1.fffffep127f) acc += cs_term(i, cs_bits(orc_rcp(x))); break;
+      case 3: if (x >= 0x1p-126f && x <= 0x1.fffffep127f) acc += cs_term(i, cs_bits(orc_rsqrt(x))); break;
+      case 4: {
+        float yy = u2f(orc_lowbias32(b)), xx = u2f(orc_lowbias32(b ^ 0x9e3779b9u));
+        if (fabsf(yy) <= 0x1.fffffep127f && fabsf(xx) <= 0x1.fffffep127f)
+          acc += cs_term(i, cs_bits(orc_atan2_turns(yy, xx)));
+        break;
+      }
+      case 5: acc += cs_term(i, orc_lowbias32(b)); break;
+      default: break;
+    }
+  }
+  return acc;
+}

@@ -108,4 +108,5 @@ int orc_zk_probes(const float duv[4], float u, float v, float uk[16], float vk[1
                   uint32_t* flags);
 void orc_zk_lod(float A, int32_t* kz, float* t);
 float orc_zk_count(uint32_t w, float nt, float p);
+uint64_t orc_contract_checksum(int32_t fn, uint64_t lo, uint64_t hi);
 #endif
