@@ -98,3 +98,35 @@ def test_negative_zero_normal_frames_agree(orc):
     g["nrm"][0, 2] = np.float32(-1e-30)       # same frame branch (negative), same geometry to fp32
     r_tiny = orc.eval(g, sc_n)[0]
     assert r_neg[0, 0] > 0 and abs(r_neg[0, 0] / r_tiny[0, 0] - 1) < 1e-5
+
+
+@pytest.mark.parametrize("ndf", ["ggx", "beckmann"])
+@pytest.mark.parametrize("alpha", [0.1, 0.35, 0.8])
+def test_white_furnace_of_the_smooth_model(orc, ndf, alpha):
+    """with F = 1, the smooth microfacet BRDF the glints
+    converge to (D from the oracle's ratio, the oracle's height-correlated G2)
+    reflects at most 1 + 2 % of the incoming energy:
+    int D(h) G2(wi, wo) / (4 n.wi) dwo <= 1.02. (Single scattering loses energy:
+    at normal incidence the part of the NDF beyond theta_h = 45 deg reflects
+    below the horizon, 1 - 1/(alpha^2 + 1) of it for GGX.)"""
+    Dn = 1.0 / (math.pi * alpha * alpha)
+    for th_i in (0.0, 0.5, 1.0, 1.3):
+        wi = np.array([math.sin(th_i), 0.0, math.cos(th_i)])
+        n_t, n_p = 160, 240
+        ths = (np.arange(n_t) + 0.5) * (math.pi / 2) / n_t
+        phs = (np.arange(n_p) + 0.5) * 2 * math.pi / n_p
+        total = 0.0
+        for th in ths:
+            for ph in phs:
+                wo = np.array([math.sin(th) * math.cos(ph), math.sin(th) * math.sin(ph), math.cos(th)])
+                h = wi + wo
+                h /= np.linalg.norm(h)
+                D = Dn * orc.ratio(ndf, alpha, alpha, *h)
+                G2 = orc.smith_g2(ndf, alpha, alpha, wi, wo)
+                total += D * G2 / (4 * wi[2]) * math.sin(th)
+        total *= (math.pi / 2 / n_t) * (2 * math.pi / n_p)
+        assert total <= 1.02, (ndf, alpha, th_i, total)
+        if th_i == 0.0 and ndf == "ggx" and alpha <= 0.35:   # G2 ~ 1: the projected NDF mass within 45 deg
+            assert 0.9 / (alpha * alpha + 1) < total <= 1.0 / (alpha * alpha + 1) + 5e-3, (alpha, total)
+        if alpha <= 0.35 and th_i <= 1.0:
+            assert total > 0.75, (ndf, alpha, th_i, total)

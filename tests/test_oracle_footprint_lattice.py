@@ -264,3 +264,26 @@ def test_lattice_smaller_max_ratio_level(orc, K):
         assert (fl == 4) == (r > 2.0 ** K)
         if r >= 2.0 ** K:
             assert orc.lattice(P, r, psi, K)[:4] == orc.lattice(P, 2.0 ** K, psi, K)[:4]
+
+
+def test_call_budget_is_48_draws_whatever_the_footprint(orc):
+    """SURVEY 8c-2 "call budget": every active (pixel, light) evaluates
+    exactly 4 grids x 3 texels x 4 nodes = 48 draws, whatever the footprint's
+    size or anisotropy: the 48 draw words of a record are all computed (no
+    zero left from the zero-filled record beyond chance); the 12 draws of each
+    weighted slot are distinct (slots merged at ring 0 keep zero weight and
+    repeat the key of the slot they merged into)."""
+    from paper_2306_05051_b200 import synth
+    gb = synth.random_gbuffer(40, 50, seed=48)
+    sc = synth.random_scene(48, n_lights=2)
+    _, fl, rec = orc.eval(gb, sc, debug=True)
+    active = rec["light_active"] == 1
+    assert active.sum() > 500
+    h = rec["hash"][active]
+    assert h.shape[1] == 48
+    nonzero = (h != 0).sum(1)
+    assert nonzero.min() >= 47
+    w = rec["w"][active]
+    for row, ww in zip(h, w):
+        words = [x for s in range(4) if ww[s] > 0 for x in row[s * 12:(s + 1) * 12].tolist()]
+        assert len(set(words)) >= len(words) - 1
