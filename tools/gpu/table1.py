@@ -107,9 +107,24 @@ def main():
         elev_rows.append(dict(elev=e, valid=valid, **{f"{k}_ms": v for k, v in res.items()}))
         lines.append(f"| {e:g} | {valid} | {res['ours']:.3f} | {valid / res['ours'] / 1e-3:.3e} | {res['zk']:.3f} | "
                      f"{valid / res['zk'] / 1e-3:.3e} | {res['zk'] / res['ours']:.2f} |")
+    # the C5 zoom path (1080p, 4 lights): cost along a x10^6 change of footprint area
+    lines += ["", "C5 zoom path at 1920x1080, 4 lights (ms per frame; area x10^6 from frame 0 to 63):", "",
+              "| frame | ours ms | zk ms | zk / ours |", "|---|---|---|---|"]
+    zoom_rows = []
+    for f in range(0, 64, 9):
+        fr = synth.c5(f, 1920, 1080, device=dev)
+        res = {}
+        for method in ("ours", "zk"):
+            fr.scene.method = method
+            res[method] = time_frame(ctx, fr.gbuf, fr.scene, a.reps)
+        zoom_rows.append(dict(frame=f, **{f"{k}_ms": v for k, v in res.items()}))
+        lines.append(f"| {f} | {res['ours']:.3f} | {res['zk']:.3f} | {res['zk'] / res['ours']:.2f} |")
+    o = [r["ours_ms"] for r in zoom_rows]
+    z = [r["zk_ms"] for r in zoom_rows]
+    lines.append(f"| max / min | {max(o) / min(o):.2f} | {max(z) / min(z):.2f} | |")
     with open(a.out + ".json", "w") as f:
-        json.dump(dict(densities=DENSITIES, rows=rows, c2_elevations=elev_rows, device=torch.cuda.get_device_name(0)), f,
-                  indent=1)
+        json.dump(dict(densities=DENSITIES, rows=rows, c2_elevations=elev_rows, c5_zoom=zoom_rows,
+                       device=torch.cuda.get_device_name(0)), f, indent=1)
     with open(a.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
