@@ -30,6 +30,11 @@ __global__ void k(uint32_t* out, uint32_t seed) {
       if (OP == 10) { v[c] = v[c] + (v[c] >> 15); v[c] = v[c] * 0x846ca68bU + seed; }
       if (OP == 11) { v[c] = v[c] ^ (v[c] >> 15); v[c] = v[c] * 0x846ca68bU + seed; }
       if (OP == 12) { v[c] = v[c] * 0x846ca68bU + seed; }
+      if (OP == 13) asm volatile("rsqrt.approx.f32 %0, %0;" : "+f"(f[c]));
+      if (OP == 14) asm volatile("{.reg .f32 t; rcp.approx.f32 t, %0; add.f32 %0, t, %1;}" : "+f"(f[c]) : "f"(f[(c + 1) % CH]));
+      if (OP == 15) asm volatile("ex2.approx.f32 %0, %0;" : "+f"(f[c]));
+      if (OP == 16) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(f[c]) : "f"(f[(c + 3) % CH]), "f"(f[(c + 5) % CH]));
+      if (OP == 17) { extern __shared__ float sm[]; f[c] += sm[(v[c] + c * 33) & 4095]; v[c] += 0x9e3779b9u; }
     }
   }
   uint32_t acc = 0;
@@ -41,11 +46,12 @@ __global__ void k(uint32_t* out, uint32_t seed) {
 template <int OP>
 float run(const char* name, int sms, uint32_t* d) {
   dim3 grid(sms * 4), block(512);
-  k<OP><<<grid, block>>>(d, 3);
+  const size_t smem = OP == 17 ? 16384 : 0;
+  k<OP><<<grid, block, smem>>>(d, 3);
   cudaEvent_t a, b;
   cudaEventCreate(&a); cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<OP><<<grid, block>>>(d, 3);
+  k<OP><<<grid, block, smem>>>(d, 3);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
@@ -60,7 +66,7 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   uint32_t* d; cudaMalloc(&d, sizeof(uint32_t) * sms * 4 * 512);
   run<0>("LOP3", sms, d);
-  run<1>("SHF (shr)", sms, d);
+  run<1>("shr+xor+add step (3 inst)", sms, d);
   run<2>("IMAD (mad.lo imm)", sms, d);
   run<3>("IMAD.HI (mad.hi)", sms, d);
   run<4>("FFMA (reg)", sms, d);
@@ -72,5 +78,10 @@ int main() {
   run<10>("add-shift + IMAD (2 ops?)", sms, d);
   run<11>("xor-shift + IMAD (3 ops)", sms, d);
   run<12>("IMAD only", sms, d);
+  run<13>("MUFU.RSQ", sms, d);
+  run<14>("MUFU.RCP (+FADD)", sms, d);
+  run<15>("MUFU.EX2", sms, d);
+  run<16>("FMNMX3 (3-input max)", sms, d);
+  run<17>("LDS (+FADD, IADD)", sms, d);
   return 0;
 }
