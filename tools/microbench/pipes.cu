@@ -34,6 +34,8 @@ __global__ void k(uint32_t* out, uint32_t seed) {
       if (OP == 14) asm volatile("{.reg .f32 t; rcp.approx.f32 t, %0; add.f32 %0, t, %1;}" : "+f"(f[c]) : "f"(f[(c + 1) % CH]));
       if (OP == 15) asm volatile("ex2.approx.f32 %0, %0;" : "+f"(f[c]));
       if (OP == 16) asm volatile("max.f32 %0, %0, %1, %2;" : "+f"(f[c]) : "f"(f[(c + 3) % CH]), "f"(f[(c + 5) % CH]));
+      if (OP == 18) asm volatile("{.reg .pred p; add.u32 %1, %1, %2; setp.le.u32 p, %1, %2; @p fma.rn.f32 %0, %0, %3, %3;}" : "+f"(f[c]), "+r"(v[c]) : "r"(seed), "f"(0.5f));
+      if (OP == 19) asm volatile("{add.u32 %1, %1, %2; fma.rn.f32 %0, %0, %3, %3;}" : "+f"(f[c]), "+r"(v[c]) : "r"(seed), "f"(0.5f));
       if (OP == 17) { extern __shared__ float sm[]; f[c] += sm[(v[c] + c * 33) & 4095]; v[c] += 0x9e3779b9u; }
     }
   }
@@ -83,5 +85,7 @@ int main() {
   run<15>("MUFU.EX2", sms, d);
   run<16>("FMNMX3 (3-input max)", sms, d);
   run<17>("LDS (+FADD, IADD)", sms, d);
+  run<18>("IADD + ISETP + @p FFMA (3 inst)", sms, d);
+  run<19>("IADD + FFMA (2 inst, control)", sms, d);
   return 0;
 }
