@@ -133,12 +133,6 @@ __device__ __forceinline__ void normalize3(float& x, float& y, float& z) {
   const float inv = rsqrt_c(dot3(x, y, z, x, y, z));
   x = x * inv; y = y * inv; z = z * inv;
 }
-// hide a value from the optimiser (keeps pre-multiplied hash seeds from being
-// re-factored into an extra multiply per draw)
-__device__ __forceinline__ uint32_t opaque(uint32_t x) {
-  asm volatile("" : "+r"(x));
-  return x;
-}
 
 // Gate parameters of one grid (Eq. 16-17, readings R-1..R-4). DESIGN §4.3 S6.
 struct Gate {

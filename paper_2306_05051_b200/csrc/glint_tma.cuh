@@ -1,8 +1,9 @@
 // glint_tma.cuh -- minimal sm_100a bulk-copy (TMA 1-D) + mbarrier helpers.
 //
-// A block streams its next tile of G-buffer pixels (5 planes x 256 float4)
-// from HBM into shared memory with cp.async.bulk while it shades the current
-// tile; completion is tracked by a transaction-count mbarrier per buffer.
+// A block streams tiles of G-buffer pixels (5 planes x kTile float4) from HBM
+// into a ring of shared-memory stages with cp.async.bulk while it shades the
+// current one; completion is tracked by a transaction-count mbarrier per stage
+// (glint_kernel.cu).
 #pragma once
 #include <stdint.h>
 
