@@ -573,3 +573,30 @@ def test_host_entry_pitched_views(ctx):
     out_d = pkg.glint_eval(ctx, dev_view, fr.scene)
     torch.cuda.synchronize()
     assert torch.equal(out_h.view(torch.int32), out_d.cpu().view(torch.int32))
+
+
+@pytest.mark.timeout(600)
+def test_max_size_launch_16k_squared(ctx):
+    """One launch over a 16384 x 16384 G-buffer (2.7e8 pixels, 21 GB of planes,
+    > 2^18 tiles, 64-bit offsets): a 1024^2 C2 crop tiled 16 x 16, so every
+    pixel's output must equal the crop's own output (all 2.7e8 checked), and
+    sampled pixels equal the oracle."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c2(30, window=(200, 1224, 400, 1424), device="cuda")
+    small = pkg.glint_eval(ctx, fr.gbuf, fr.scene)
+    big = synth.GBuffer(*[p.repeat(16, 16, 1) for p in fr.gbuf.planes()])
+    assert big.height == 16384 and big.width == 16384
+    out = pkg.glint_eval(ctx, big, fr.scene)
+    torch.cuda.synchronize()
+    ref = small.view(torch.int32).repeat(16, 16, 1)
+    assert torch.equal(out.view(torch.int32), ref)
+    del big, ref
+    g = torch.Generator().manual_seed(16)
+    idx = torch.randint(0, 1024 * 1024, (600,), generator=g)
+    sub = fr.gbuf.take(idx).to("cpu")
+    rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+    compare_radiance(small.reshape(-1, 4)[idx.to("cuda")], rgb_o, fl_o, "16k source crop")
+    del out
+    torch.cuda.empty_cache()
