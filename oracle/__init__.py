@@ -89,7 +89,7 @@ def lib():
             L.orc_log2_1mp.argtypes = [C.c_float]; L.orc_log2_1mp.restype = C.c_float
             L.orc_atan2_turns.argtypes = [C.c_float, C.c_float]; L.orc_atan2_turns.restype = C.c_float
             L.orc_lowbias32.argtypes = [C.c_uint32]; L.orc_lowbias32.restype = C.c_uint32
-            L.orc_lowbias32_tail.argtypes = [C.c_uint32]; L.orc_lowbias32_tail.restype = C.c_uint32
+            L.orc_draw_hash.argtypes = [C.c_uint32]; L.orc_draw_hash.restype = C.c_uint32
             L.orc_footprint.argtypes = [fp, fp, fp, fp]; L.orc_footprint.restype = C.c_int
             i4p = C.POINTER(C.c_int32)
             L.orc_lattice.argtypes = [C.c_float, C.c_float, C.c_float, C.c_int32, i4p, i4p, i4p, fp,
@@ -243,8 +243,8 @@ def lowbias32(x: int) -> int:
     return lib().orc_lowbias32(x & 0xFFFFFFFF)
 
 
-def lowbias32_tail(x: int) -> int:
-    return lib().orc_lowbias32_tail(x & 0xFFFFFFFF)
+def draw_hash(x: int) -> int:
+    return lib().orc_draw_hash(x & 0xFFFFFFFF)
 
 
 def footprint(duv):

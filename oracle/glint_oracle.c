@@ -189,11 +189,15 @@ uint32_t orc_lowbias32(uint32_t x) {
   return x;
 }
 
-/* the last four steps of lowbias32; the per-draw hash is h = tail(hs + ka)
- * of the spatial seed hs and the angular seed ka (both full lowbias32 outputs) */
-uint32_t orc_lowbias32_tail(uint32_t x) {
+/* the per-draw hash h = draw_hash(hs + ka) of the spatial seed hs and the
+ * angular seed ka (both full lowbias32 outputs): the last four steps of
+ * lowbias32 with the middle xor-shift replaced by an xor-rotate by 15
+ * (reading R-23b: the shift leaves chi-square-detectable dependence between the
+ * 4 node draws of a texel, whose sums differ by fixed offsets; the rotation
+ * feeds the top bits of x*C1 back into the low bits and removes it) */
+uint32_t orc_draw_hash(uint32_t x) {
   x *= 0x7feb352dU;
-  x ^= x >> 15;
+  x ^= (x >> 15) | (x << 17);
   x *= 0x846ca68bU;
   x ^= x >> 16;
   return x;
@@ -850,7 +854,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       for (int k = 0; k < NS; ++k) {
         double Cik = 0.0;
         for (int jn = 0; jn < 4; ++jn) {
-          uint32_t h = orc_lowbias32_tail(hs[i][k] + ka[jn]);
+          uint32_t h = orc_draw_hash(hs[i][k] + ka[jn]);
           float c = sc->sampler == 1 ? exact_count(h, n[i], p) : orc_gated_count(h, T, sig, m1, cap);
           if (rc) { rc->hash[i*12 + k*4 + jn] = h; rc->count[i*12 + k*4 + jn] = c; }
           Cik += vj[jn] * (double)c;

@@ -90,7 +90,7 @@ float orc_rcp(float x);
 float orc_log2_1mp(float p);
 float orc_atan2_turns(float y, float x);
 uint32_t orc_lowbias32(uint32_t x);
-uint32_t orc_lowbias32_tail(uint32_t x);
+uint32_t orc_draw_hash(uint32_t x);
 int orc_footprint(const float duv[4], float* P, float* r, float* psi);
 int orc_lattice(float P, float r, float psi, int32_t K, int32_t ls[4], int32_t lr[4],
                 int32_t jo[4], float w[4], uint32_t* flags);

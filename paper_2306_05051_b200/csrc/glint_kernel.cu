@@ -304,7 +304,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   for (int i = 0; i < 4; ++i) n[i] = sl[i].w * (N * pow2i(sl[i].ls));
 
   // ---------------- S3 + S4a: grid transform, simplex, spatial seeds (12)
-  // hsC = hs * C1: the draw hash tail(hs + ka) starts with (hs + ka) * C1 =
+  // hsC = hs * C1: the draw hash draw_hash(hs + ka) starts with (hs + ka) * C1 =
   // hsC + kaC, one add per draw.
   const uint32_t so = lowbias32(__float_as_uint(uvm.z) ^ seed_h);
   uint32_t hsC[12];
@@ -519,7 +519,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
           for (int jn = 0; jn < 4; ++jn) {
             uint32_t y = hC + kaC[jn];
-            y ^= y >> 15;
+            y ^= __funnelshift_r(y, y, 15);
             y *= 0x846ca68bU;
             const uint32_t s16 = y >> 16;
             const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
@@ -557,7 +557,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
           uint32_t y = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
-          y ^= y >> 15;
+          y ^= __funnelshift_r(y, y, 15);           // xor-rotate (R-23b)
           y *= 0x846ca68bU;                              // y: gate bits 9..31
           const uint32_t s16 = y >> 16;                  // h = y ^ (y >> 16): quantile bits 2..13
           const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));

@@ -85,7 +85,12 @@ def test_bilinear_partition_and_vertices(orc):
 @pytest.mark.parametrize("draws", [64, 160])
 def test_ablations_have_the_same_expectation(orc, draws):
     """All three distributions give an unbiased D_P with the exact sampler:
-    mean over seeds of C equals N P p (the draw count is the only change)."""
+    mean over seeds of C equals N P p (the draw count is the only change), so
+    the radiance means agree. Per seed, the 16 pixels (same footprint and h)
+    are averaged; the paired per-seed difference between the two modes must be
+    within 4 standard errors of 0 (a derived bound: one 150-seed mean has a
+    relative standard error of ~2-3% here, so a fixed 3% tolerance would be a
+    one-sigma test) and the relative gap below 8%."""
     rng = np.random.default_rng(34)
     fr = synth.c1("ggx", "az90")
     gb = fr.gbuf.crop(0, 4, 0, 4)
@@ -101,7 +106,9 @@ def test_ablations_have_the_same_expectation(orc, draws):
         for sd in range(150):
             sc = synth.SceneParams(**{**fr.scene.__dict__, "seed": 500 + sd, "draws": mode})
             rgb, _, _ = orc.eval(gb, sc, sampler="exact", threads=1)
-            Cs.append(rgb[:, 0])
-        ms.append(np.mean(Cs, 0))
-    # same footprint and h in all 16 pixels: compare the pixel-averaged means
-    assert abs(ms[0].mean() / ms[1].mean() - 1) < 0.03, (ms[0].mean(), ms[1].mean())
+            Cs.append(rgb[:, 0].mean())
+        ms.append(np.array(Cs))
+    d = ms[0] - ms[1]
+    se = d.std(ddof=1) / np.sqrt(len(d))
+    assert abs(d.mean()) < 4 * se, (ms[0].mean(), ms[1].mean(), se)
+    assert abs(ms[0].mean() / ms[1].mean() - 1) < 0.08, (ms[0].mean(), ms[1].mean())

@@ -11,7 +11,10 @@ measure between every pair of the 4 nodes (over 10^6 texel seeds)
   * the Pearson correlation of the gate indicators at P>=1 = 1/4 and of the
     quantiles (effect size; noise ~1e-3).
 Candidates (ALU ops per draw in the kernel's draw loop, hash part only):
-  current   tail(hs + ka), gate on y = u*C2, index (y ^ y>>16)   -- 5 ops
+  current   draw_hash(hs + ka): t = x*C1; u = t ^ rotr(t, 15); y = u*C2;
+            gate on y, index (y ^ y>>16)                          -- 5 ops
+  shift15   the same with lowbias32's xor-shift u = t ^ t>>15
+            (the round-1 design before R-23b)                    -- 5 ops
   xor_mul   (hs ^ ka) * C2                                        -- 2 ops
   premix    lowbias32-like: x = hs + ka; x ^= x>>16; then tail    -- 7 ops
   xor_tail  tail(hs ^ ka) (no pre-multiplication possible)        -- 6 ops
@@ -38,15 +41,18 @@ def lb(x):
     return x ^ (x >> U(16))
 
 
-def tail3(x):                     # t = x*C1; u = t ^ t>>15; y = u*C2
+def tail3(x, rotate=False):       # t = x*C1; u = t ^ t>>15 (or rotr 15); y = u*C2
     t = (x & M) * C1 & M
-    u = t ^ (t >> U(15))
+    u = t ^ ((((t >> U(15)) | (t << U(17))) & M) if rotate else (t >> U(15)))
     return (u * C2) & M, u
 
 
 def cand(name, hs, ka):
     """-> (y: gate word (bits 9..31), q: quantile index 0..4095)."""
     if name == "current":
+        y, _ = tail3(hs + ka, rotate=True)
+        return y, ((y ^ (y >> U(16))) >> U(2)) & U(4095)
+    if name == "shift15":
         y, _ = tail3(hs + ka)
         return y, ((y ^ (y >> U(16))) >> U(2)) & U(4095)
     if name == "xor_mul":
@@ -65,7 +71,7 @@ def cand(name, hs, ka):
     raise ValueError(name)
 
 
-OPS = {"current": 5, "xor_mul": 2, "premix": 7, "xor_tail": 6, "u_index": 4}
+OPS = {"current": 5, "shift15": 5, "xor_mul": 2, "premix": 7, "xor_tail": 6, "u_index": 4}
 
 
 def battery(name, n, cells, seed=0):
