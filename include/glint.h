@@ -49,6 +49,7 @@ extern "C" {
 #define GLINT_ELIMIT -4   /* width*height or pitch*height >= 2^31 pixels */
 #define GLINT_ECUDA -5    /* a CUDA runtime call failed; see glint_last_cuda_error() */
 #define GLINT_ENOMEM -6   /* host or device allocation failed */
+#define GLINT_EALIAS -7   /* glint_eval_batch: an output overlaps an input plane or another output */
 
 /* per-pixel output flags, stored as the bit pattern of out[pixel].w */
 #define GLINT_FLAG_INVALID 1u        /* meta bit0 clear: pixel not shaded */
@@ -173,6 +174,26 @@ int glint_destroy(glint_ctx* ctx);   /* waits for the device (cudaDeviceSynchron
  * must not be replayed concurrently with itself. */
 int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
                void* out, int64_t out_pitch, glint_debug_rec* dbg, void* stream);
+
+/* Evaluate n_frames independent frames (C2's elevation set, C4's jittered
+ * frames, C5's zoom path: P:L1010-1032 time whole frames): frame f is exactly
+ * glint_eval(ctx, &gbs[f], &scenes[f], outs[f], out_pitches[f], NULL, stream),
+ * bit for bit. The launches are chained with programmatic dependent launch:
+ * frame f+1's blocks start on the SMs that frame f's blocks free at its tail
+ * instead of after frame f completes ("frame batching").
+ * This is only correct because the frames do not depend on each other, so the
+ * call checks it: every output range [outs[f], outs[f] + ((h-1)*out_pitch + w)
+ * float4) must be disjoint from every input plane range of every frame and
+ * from every other output, else GLINT_EALIAS (nothing launched). Frame 0
+ * waits for all prior work on `stream` like glint_eval; work enqueued on
+ * `stream` after the call sees every frame complete (each frame's grid waits
+ * for its predecessor before it exits). Arguments: host arrays of n_frames
+ * entries (gbs, scenes, outs, out_pitches), device buffers behind them as for
+ * glint_eval; n_frames = 0 is a no-op; empty frames are skipped. Every frame
+ * is validated before the first launch; an error launches nothing. No debug
+ * records (use glint_eval). Graph-capturable; one scheduler slot per frame. */
+int glint_eval_batch(const glint_ctx* ctx, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
+                     void* const* outs, const int64_t* out_pitches, void* stream);
 
 /* End-to-end entry with HOST buffers: copies the planes host->device, runs the
  * kernel and copies the radiance device->host, pipelined over row chunks on

@@ -15,14 +15,16 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GLINT_LIB") or os.path.join(_HERE, "libglint.so")
 
-GLINT_OK, GLINT_EINVAL, GLINT_EALIGN, GLINT_EDEVICE, GLINT_ELIMIT, GLINT_ECUDA, GLINT_ENOMEM = 0, -1, -2, -3, -4, -5, -6
+GLINT_OK, GLINT_EINVAL, GLINT_EALIGN, GLINT_EDEVICE, GLINT_ELIMIT, GLINT_ECUDA, GLINT_ENOMEM, GLINT_EALIAS = \
+    0, -1, -2, -3, -4, -5, -6, -7
 FLAG_INVALID, FLAG_DEGENERATE, FLAG_RATIO_CLAMPED, FLAG_P_CLAMPED, FLAG_UV_RANGE = 1, 2, 4, 8, 16
 MAX_LIGHTS = 16
 ZQ = 4096
 NANG = 256
 
 EXPORTS = ["glint_version", "glint_strerror", "glint_last_cuda_error", "glint_build_tables", "glint_create",
-           "glint_destroy", "glint_eval", "glint_eval_host", "glint_get_tables", "glint_launch_count"]
+           "glint_destroy", "glint_eval", "glint_eval_batch", "glint_eval_host", "glint_get_tables",
+           "glint_launch_count"]
 
 
 class GlintError(RuntimeError):
@@ -89,6 +91,9 @@ def lib():
         L.glint_eval.argtypes = [C.c_void_p, C.POINTER(glint_gbuffer), C.POINTER(glint_scene), C.c_void_p,
                                  C.c_int64, C.c_void_p, C.c_void_p]
         L.glint_eval.restype = C.c_int
+        L.glint_eval_batch.argtypes = [C.c_void_p, C.c_int, C.POINTER(glint_gbuffer), C.POINTER(glint_scene),
+                                       C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_void_p]
+        L.glint_eval_batch.restype = C.c_int
         L.glint_eval_host.argtypes = [C.c_void_p, C.POINTER(glint_gbuffer), C.POINTER(glint_scene), C.c_void_p,
                                       C.c_int64, C.c_void_p]
         L.glint_eval_host.restype = C.c_int
@@ -231,6 +236,36 @@ def glint_eval(ctx: Context, gb, scene, out=None, debug: bool = False, stream=No
         rec = dbg.cpu().numpy().view(np.uint8)[: n * DEBUG_REC_BYTES].view(DEBUG_REC_DTYPE)
         return out, rec.reshape(g.width * g.height, sc.n_lights)
     return out
+
+
+def glint_eval_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
+    """Shade independent device-resident frames with one call (the launches
+    are chained with programmatic dependent launch; include/glint.h). Frame f's
+    result equals glint_eval(ctx, gbs[f], scenes[f]) bit for bit. Returns the
+    list of (H, W, 4) radiance tensors."""
+    import torch
+    n = len(gbs)
+    if len(scenes) != n or (outs is not None and len(outs) != n):
+        raise ValueError("gbs, scenes and outs must have the same length")
+    if n == 0:
+        return []
+    dev = gbs[0].planes()[0].device
+    if any(g.planes()[0].device != dev for g in gbs) or dev.type != "cuda":
+        raise ValueError("glint_eval_batch needs CUDA tensors on one device")
+    G = (glint_gbuffer * n)(*[_gbuffer_struct(g) for g in gbs])
+    S = (glint_scene * n)(*[scene_struct(sc) for sc in scenes])
+    if outs is None:
+        outs = [torch.empty((G[f].height, G[f].width, 4), dtype=torch.float32, device=dev) for f in range(n)]
+    for o in outs:
+        if o.stride(2) != 1 or o.stride(1) != 4:
+            raise ValueError("out must be a contiguous-row float4 tensor")
+    P = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    Q = (C.c_int64 * n)(*[o.stride(0) // 4 for o in outs])
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    rc = lib().glint_eval_batch(ctx.handle, n, G, S, P, Q, C.c_void_p(s.cuda_stream))
+    if rc:
+        raise GlintError(rc, "glint_eval_batch")
+    return outs
 
 
 def glint_eval_host(ctx: Context, gb, scene, out=None, stream=None):

@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "../../include/glint.h"
 #include "glint_kernel.h"
@@ -51,6 +52,7 @@ extern "C" int glint_version(void) { return GLINT_VERSION; }
 extern "C" const char* glint_strerror(int code) {
   switch (code) {
     case GLINT_OK: return "ok";
+    case GLINT_EALIAS: return "an output overlaps an input plane or another output of the batch";
     case GLINT_EINVAL: return "invalid argument";
     case GLINT_EALIGN: return "pointer not 16-byte aligned or pitch < width";
     case GLINT_EDEVICE: return "no suitable sm_100 device / context-device mismatch";
@@ -280,6 +282,58 @@ extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const gli
   int64_t n_pix = (int64_t)gb->width * gb->height;
   GL_CUDA(glint::launch_eval(k, grid_for(c, n_pix), dbg != nullptr, (cudaStream_t)stream));
   const_cast<glint_ctx*>(c)->launches++;
+  return GLINT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// glint_eval_batch: independent frames, launches chained with programmatic
+// dependent launch (frame f+1 fills the SMs frame f frees at its tail)
+// ---------------------------------------------------------------------------
+namespace {
+struct Range { uintptr_t lo, hi; };   // [lo, hi) bytes
+Range plane_range(const void* p, int64_t pitch, int w, int h) {
+  const uintptr_t lo = (uintptr_t)p;
+  return {lo, lo + (uintptr_t)(((int64_t)(h - 1) * pitch + w) * 16)};
+}
+bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi; }
+}  // namespace
+
+extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
+                                void* const* outs, const int64_t* out_pitches, void* stream) {
+  if (!c || n_frames < 0) return GLINT_EINVAL;
+  if (n_frames == 0) return GLINT_OK;
+  if (!gbs || !scenes || !outs || !out_pitches) return GLINT_EINVAL;
+  std::vector<Range> outr, inr;
+  for (int f = 0; f < n_frames; ++f) {
+    int rc = validate_scene(&scenes[f]);
+    if (rc) return rc;
+    rc = validate_gbuffer(&gbs[f], out_pitches[f]);
+    if (rc) return rc;
+    const glint_gbuffer& g = gbs[f];
+    if (g.width == 0 || g.height == 0) continue;
+    if (!outs[f]) return GLINT_EINVAL;
+    if (!aligned16(outs[f])) return GLINT_EALIGN;
+    outr.push_back(plane_range(outs[f], out_pitches[f], g.width, g.height));
+    for (const void* p : {g.duv, g.uvm, g.nrm, g.pos, g.mat}) inr.push_back(plane_range(p, g.pitch, g.width, g.height));
+  }
+  for (size_t a = 0; a < outr.size(); ++a) {
+    for (const Range& r : inr)
+      if (overlap(outr[a], r)) return GLINT_EALIAS;
+    for (size_t b = a + 1; b < outr.size(); ++b)
+      if (overlap(outr[a], outr[b])) return GLINT_EALIAS;
+  }
+  int cur = -1;
+  GL_CUDA(cudaGetDevice(&cur));
+  if (cur != c->device) return GLINT_EDEVICE;
+  bool first = true;
+  for (int f = 0; f < n_frames; ++f) {
+    const glint_gbuffer& g = gbs[f];
+    if (g.width == 0 || g.height == 0) continue;
+    glint::KParams k = make_params(c, &g, &scenes[f], outs[f], out_pitches[f], nullptr);
+    GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)g.width * g.height), false, (cudaStream_t)stream, !first));
+    const_cast<glint_ctx*>(c)->launches++;
+    first = false;
+  }
   return GLINT_OK;
 }
 

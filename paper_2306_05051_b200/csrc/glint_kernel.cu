@@ -652,6 +652,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   };
   auto claim = [&]() -> int64_t { return (int64_t)gridDim.x + (int64_t)atomicAdd(&prm.sched[0], 1ull); };
 
+  // the next frame of a glint_eval_batch may launch now: its blocks fill the
+  // SMs this grid's blocks free at its tail (frames of a batch are independent)
+  pdl_launch_dependents();
   if (tid == 0) {
     mbar_init(tbar, 1);
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); s_done[s] = 0u; }
@@ -720,11 +723,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       prm.sched[1] = 0ull;
       __threadfence();
     }
+    // a batch frame completes only after the frame before it: work that
+    // follows the batch in the stream then sees every frame complete
+    pdl_wait_prerequisites();
   }
 }
 
 template <bool DEBUG, bool TMA, int MODE>
-static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream) {
+static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, bool pdl) {
   const size_t smem = TMA ? kSmemTma : kSmemTables;
   static bool configured = false;
   if (!configured) {
@@ -733,19 +739,37 @@ static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  glint_eval_kernel<DEBUG, TMA, MODE><<<grid, kBlock, smem, stream>>>(prm);
-  return cudaGetLastError();
+  if (!pdl) {
+    glint_eval_kernel<DEBUG, TMA, MODE><<<grid, kBlock, smem, stream>>>(prm);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kBlock);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, glint_eval_kernel<DEBUG, TMA, MODE>, prm);
 }
 
-cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream) {
+cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream, bool pdl) {
   const bool tma = (prm.pitch == prm.width) && (((uintptr_t)prm.duv | (uintptr_t)prm.uvm | (uintptr_t)prm.nrm |
                                                   (uintptr_t)prm.pos | (uintptr_t)prm.mat) % 16 == 0);
-  if (debug) return tma ? launch_t<true, true, 0>(prm, grid, stream) : launch_t<true, false, 0>(prm, grid, stream);
+  if (debug)
+    return tma ? launch_t<true, true, 0>(prm, grid, stream, pdl) : launch_t<true, false, 0>(prm, grid, stream, pdl);
   switch (prm.sc.eval_mode) {
-    case 1: return tma ? launch_t<false, true, 1>(prm, grid, stream) : launch_t<false, false, 1>(prm, grid, stream);
-    case 2: return tma ? launch_t<false, true, 2>(prm, grid, stream) : launch_t<false, false, 2>(prm, grid, stream);
-    case 3: return tma ? launch_t<false, true, 3>(prm, grid, stream) : launch_t<false, false, 3>(prm, grid, stream);
-    default: return tma ? launch_t<false, true, 0>(prm, grid, stream) : launch_t<false, false, 0>(prm, grid, stream);
+    case 1:
+      return tma ? launch_t<false, true, 1>(prm, grid, stream, pdl) : launch_t<false, false, 1>(prm, grid, stream, pdl);
+    case 2:
+      return tma ? launch_t<false, true, 2>(prm, grid, stream, pdl) : launch_t<false, false, 2>(prm, grid, stream, pdl);
+    case 3:
+      return tma ? launch_t<false, true, 3>(prm, grid, stream, pdl) : launch_t<false, false, 3>(prm, grid, stream, pdl);
+    default:
+      return tma ? launch_t<false, true, 0>(prm, grid, stream, pdl) : launch_t<false, false, 0>(prm, grid, stream, pdl);
   }
 }
 

@@ -52,7 +52,7 @@ struct KParams {
   glint_scene sc;
 };
 
-cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream);
+cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream, bool pdl = false);
 cudaError_t occupancy_blocks_per_sm(int* out);
 
 }  // namespace glint

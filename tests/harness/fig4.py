@@ -9,7 +9,7 @@ pixels with distinct object ids (independent seeds) up to ~10^8 draws and
 compared, at M = 10^4 .. 10^8, with the contract's exact law (the convolution
 of the two enumerated gated laws, oracle/stats.py) and with Binomial(24, 1/2).
 
-usage: python tools/gpu/fig4.py [--out gpurun_out/fig4] [--chunks 8]
+usage: python tests/harness/fig4.py [--out gpurun_out/fig4] [--chunks 8]
 """
 import argparse
 import json

@@ -4,7 +4,7 @@ binomial (DEBUG records, production arithmetic), compared with the contract's
 exact gated law (chi-square, enumerated by oracle/stats.py) and with the
 exact Binomial(n, p) (total variation: the approximation error Fig. 9 shows).
 
-usage: python tools/gpu/fig9.py [--out gpurun_out/fig9]
+usage: python tests/harness/fig9.py [--out gpurun_out/fig9]
 """
 import argparse
 import json
