@@ -7,7 +7,9 @@
  * light in the mirror configuration, uploads it with the CUDA runtime, calls
  * glint_eval, and prints the number of glinting pixels and a checksum of the
  * radiance. Also runs the host-buffer entry glint_eval_host and checks that
- * both entries return the same bits.
+ * both entries return the same bits, and shades two frames (the same quad
+ * under two seeds) with one glint_eval_batch call: frame 0 must equal the
+ * single glint_eval bit for bit, and an output aliasing an input is refused.
  *
  * Build: gcc -O2 -I include examples/glint_c_example.c \
  *          -L paper_2306_05051_b200 -lglint -L /usr/local/cuda/lib64 -lcudart \
@@ -85,6 +87,23 @@ int main(void) {
   float* out_h = (float*)malloc(16 * n);
   CHECK(glint_eval_host(ctx, &gh, &sc, out_h, W, NULL));
 
+  /* two independent frames in one call (launches chained on the GPU) */
+  void* dout2;
+  if (cudaMalloc(&dout2, 16 * n) != cudaSuccess) return 1;
+  glint_gbuffer gbs[2] = {gb, gb};
+  glint_scene scs[2] = {sc, sc};
+  scs[1].seed = 2;
+  void* outs[2] = {dout, dout2};
+  int64_t pitches[2] = {W, W};
+  CHECK(glint_eval_batch(ctx, 2, gbs, scs, outs, pitches, NULL));
+  float* out_b = (float*)malloc(16 * n);
+  if (cudaMemcpy(out_b, dout, 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  int batch_same = memcmp(out, out_b, 16 * n) == 0;
+  void* bad_outs[2] = {dout, dev[4]};   /* frame 1 would overwrite the material plane */
+  int alias_rc = glint_eval_batch(ctx, 2, gbs, scs, bad_outs, pitches, NULL);
+  cudaFree(dout2);
+  free(out_b);
+
   int glints = 0;
   double sum = 0.0;
   for (size_t i = 0; i < n; ++i) {
@@ -92,12 +111,13 @@ int main(void) {
     sum += out[4 * i] + out[4 * i + 1] + out[4 * i + 2];
   }
   int same = memcmp(out, out_h, 16 * n) == 0;
-  printf("glinting pixels %d of %zu, radiance sum %.9g, host entry identical %d, launches %lld\n", glints, n, sum,
-         same, (long long)glint_launch_count(ctx));
+  printf("glinting pixels %d of %zu, radiance sum %.9g, host entry identical %d, batch identical %d, "
+         "aliased batch refused %d, launches %lld\n", glints, n, sum, same, batch_same, alias_rc == GLINT_EALIAS,
+         (long long)glint_launch_count(ctx));
   CHECK(glint_destroy(ctx));
   for (int p = 0; p < 5; ++p) { cudaFree(dev[p]); free(host[p]); }
   cudaFree(dout);
   free(out);
   free(out_h);
-  return (glints > 0 && same) ? 0 : 2;
+  return (glints > 0 && same && batch_same && alias_rc == GLINT_EALIAS) ? 0 : 2;
 }
