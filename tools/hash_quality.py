@@ -20,7 +20,12 @@ Candidates (ALU ops per draw in the kernel's draw loop, hash part only):
   xor_tail  tail(hs ^ ka) (no pre-multiplication possible)        -- 6 ops
   u_index   current gate, index from u = t ^ (t>>15) bits 2..13   -- 4 ops
 
-usage: python tools/hash_quality.py [--n 1000000] [--cells 24]
+A second mode scans random node-seed offsets (`--node-pairs K`): for K random
+pairs (ka0, ka1) of lowbias32 outputs, the worst chi-square p and Cramér's V
+of the 4 contingencies between the two nodes' draws over 2^20 texel seeds,
+for `current` and for the 7-op `premix` (a full lowbias32 of the sum).
+
+usage: python tools/hash_quality.py [--n 1000000] [--cells 24] [--node-pairs 300]
 """
 import argparse
 import json
@@ -101,12 +106,43 @@ def battery(name, n, cells, seed=0):
                 max_corr_quantile=float(max(corr_q)), pairs=len(corr_g))
 
 
+def node_pair_scan(name, pairs, seed=3, n=1 << 20):
+    """Random node-seed offsets: fraction of pairs whose draws are detectably
+    dependent, and the largest effect size (Cramér's V; noise ~0.0013)."""
+    hs = lb(np.arange(n, dtype=U) * U(0x9e3779b1) + U(99))
+    rng = np.random.default_rng(seed)
+    ps, vs, worst = [], [], []
+    for _ in range(pairs):
+        ka0, ka1 = [lb(U(int(v))) for v in rng.integers(0, 2 ** 32, 2)]
+        y1, q1 = cand(name, hs, ka0)
+        y2, q2 = cand(name, hs, ka1)
+        best_p, best_v = 1.0, 0.0
+        for u, v in ((y1 >> U(28), y2 >> U(28)), (q1 >> U(8), q2 >> U(8)), (y1 >> U(28), q2 >> U(8)),
+                     (q1 & U(15), q2 & U(15))):
+            tab = np.bincount((u * U(16) + v).astype(np.int64), minlength=256).reshape(16, 16)
+            c, pv = st.chi2_contingency(tab)[:2]
+            best_p = min(best_p, float(pv))
+            best_v = max(best_v, float(np.sqrt(max(c - 225.0, 0.0) / n / 15)))
+        ps.append(best_p)
+        vs.append(best_v)
+        worst.append((best_p, (int(ka1) - int(ka0)) * 0x7feb352d & 0xFFFFFFFF))
+    ps, vs = np.array(ps), np.array(vs)
+    return dict(pairs=pairs, frac_p_lt_1e3=float((ps < 1e-3).mean()), frac_expected=1 - (1 - 1e-3) ** 4,
+                frac_p_lt_1e6=float((ps < 1e-6).mean()), max_cramers_v=float(vs.max()),
+                median_cramers_v=float(np.median(vs)), worst_offsets_D=[f"{d:08x}" for _, d in sorted(worst)[:3]])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--cells", type=int, default=24)
+    ap.add_argument("--node-pairs", type=int, default=0)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
+    if a.node_pairs:
+        for name in ("current", "premix"):
+            print(name, node_pair_scan(name, a.node_pairs), flush=True)
+        return
     res = {}
     for name in OPS:
         res[name] = battery(name, a.n, a.cells)
