@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/glint.h"
 #include "glint_device.cuh"
 #include "glint_kernel.h"
@@ -732,12 +734,19 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
 template <bool DEBUG, bool TMA, int MODE>
 static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, bool pdl) {
   const size_t smem = TMA ? kSmemTma : kSmemTables;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the dynamic shared-memory opt-in, once per (instantiation, device);
+  // concurrent first launches from several host threads may both set it
+  // (idempotent), the flag itself is atomic
+  static std::atomic<uint64_t> configured{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    configured.fetch_or(bit, std::memory_order_release);
   }
   if (!pdl) {
     glint_eval_kernel<DEBUG, TMA, MODE><<<grid, kBlock, smem, stream>>>(prm);
