@@ -172,3 +172,25 @@ def test_batch_launch_count_and_stats(ctx):
     torch.cuda.synchronize()
     assert ctx.launch_count() - n0 == 3
     assert all(np.isfinite(o[..., :3].cpu().numpy()).all() for o in outs[:3])
+
+
+def test_batches_on_concurrent_streams(ctx):
+    """Two batches in flight at once on two streams (their chains interleave
+    on the SMs; every launch has its own scheduler slot): each frame still
+    equals its glint_eval reference bit for bit."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fa = [synth.c2(e, window=(200, 456, 0, 1920), device="cuda") for e in (15, 35, 55)]
+    fb = [synth.c2(e, window=(600, 856, 0, 1920), device="cuda") for e in (25, 45, 65, 85)]
+    refs = {id(fr): pkg.glint_eval(ctx, fr.gbuf, fr.scene).clone() for fr in fa + fb}
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(3):
+        oa = [torch.full_like(refs[id(fr)], float("nan")) for fr in fa]
+        ob = [torch.full_like(refs[id(fr)], float("nan")) for fr in fb]
+        sa.wait_stream(torch.cuda.current_stream())
+        sb.wait_stream(torch.cuda.current_stream())
+        pkg.glint_eval_batch(ctx, [f.gbuf for f in fa], [f.scene for f in fa], outs=oa, stream=sa)
+        pkg.glint_eval_batch(ctx, [f.gbuf for f in fb], [f.scene for f in fb], outs=ob, stream=sb)
+        torch.cuda.synchronize()
+        for fr, o in list(zip(fa, oa)) + list(zip(fb, ob)):
+            assert _same(o, refs[id(fr)])
