@@ -56,3 +56,52 @@ def test_scene_struct_layout(glib):
     assert C.sizeof(glib._lib.glint_light) == 32
     assert C.sizeof(glib._lib.glint_scene) == 64 + 16 * 32
     assert C.sizeof(glib._lib.glint_gbuffer) == 5 * 8 + 4 + 4 + 8
+
+
+def test_batch_validation_and_alias_rules_without_gpu(glib):
+    """glint_eval_batch validates every frame and the output/input overlap
+    rule before it touches the context or the device (include/glint.h), so
+    the rules run here on fake, never dereferenced, 16-byte-aligned
+    addresses: any output overlapping any frame's input plane or another
+    output -> GLINT_EALIAS; disjoint (even adjacent) ranges pass validation
+    and only then fail on the missing device."""
+    import torch
+    L = glib.lib()
+    m = glib._lib
+    W, H, pitch = 64, 8, 64
+    plane = pitch * H * 16                      # bytes of one plane
+
+    def frame(base):
+        g = m.glint_gbuffer()
+        g.duv, g.uvm, g.nrm, g.pos, g.mat = [base + k * plane for k in range(5)]
+        g.width, g.height, g.pitch = W, H, pitch
+        return g
+
+    sc = glib._lib.scene_struct(__import__("paper_2306_05051_b200.synth", fromlist=["x"]).SceneParams())
+    G = (m.glint_gbuffer * 2)(frame(0x10000000), frame(0x20000000))
+    S = (m.glint_scene * 2)(sc, sc)
+    Q = (C.c_int64 * 2)(pitch, pitch)
+    fake_ctx = C.c_void_p(0x1000)               # validation never dereferences it
+
+    def run(o0, o1):
+        P = (C.c_void_p * 2)(o0, o1)
+        return L.glint_eval_batch(fake_ctx, 2, G, S, P, Q, None)
+
+    out = 0x30000000
+    assert run(out, 0x10000000 + 2 * plane) == m.GLINT_EALIAS          # over frame 0's nrm plane
+    assert run(out, 0x20000000 + 4 * plane + 16 * 5) == m.GLINT_EALIAS  # inside frame 1's mat plane
+    assert run(out, out) == m.GLINT_EALIAS                              # two outputs overlap
+    assert run(out, out + plane - 16) == m.GLINT_EALIAS                 # overlap by one float4
+    assert run(0x20000000 - plane + 16, out) == m.GLINT_EALIAS          # last float4 reaches frame 1's duv
+    assert run(out, out + 4 * 3) == m.GLINT_EALIGN                      # misaligned second output
+    rc = run(out, out + plane)                                          # adjacent: valid, then needs the device
+    if not torch.cuda.is_available():
+        assert rc == m.GLINT_ECUDA or rc == m.GLINT_EDEVICE
+    # frame-level validation still applies, and n_frames = 0 is a no-op
+    bad = (m.glint_scene * 2)(sc, sc)
+    bad[1].ndf_kind = 7
+    P = (C.c_void_p * 2)(out, out + plane)
+    assert L.glint_eval_batch(fake_ctx, 2, G, bad, P, Q, None) == m.GLINT_EINVAL
+    assert L.glint_eval_batch(fake_ctx, 0, None, None, None, None, None) == m.GLINT_OK
+    assert L.glint_eval_batch(None, 2, G, S, P, Q, None) == m.GLINT_EINVAL
+    assert L.glint_eval_batch(fake_ctx, -1, G, S, P, Q, None) == m.GLINT_EINVAL
