@@ -205,6 +205,17 @@ int glint_eval_batch(const glint_ctx* ctx, int n_frames, const glint_gbuffer* gb
 int glint_eval_host(glint_ctx* ctx, const glint_gbuffer* gb_host, const glint_scene* scene,
                     void* out_host, int64_t out_pitch, void* stream);
 
+/* glint_eval_host over n_frames independent frames (host arrays of n_frames
+ * entries, host buffers behind them): frame f's radiance equals
+ * glint_eval_host(ctx, &gbs_host[f], &scenes[f], outs_host[f], out_pitches[f],
+ * stream) bit for bit. The row-chunk pipeline runs continuously across the
+ * frames, so it fills and drains once per call instead of once per frame.
+ * Every frame is validated first; outputs (16-byte aligned) must not overlap
+ * any input plane or another output (GLINT_EALIAS). Synchronous, serialised
+ * per context like glint_eval_host. n_frames = 0 is a no-op. */
+int glint_eval_host_batch(glint_ctx* ctx, int n_frames, const glint_gbuffer* gbs_host, const glint_scene* scenes,
+                          void* const* outs_host, const int64_t* out_pitches, void* stream);
+
 /* Copies of the device-resident tables (host pointers), for parity tests. */
 int glint_get_tables(const glint_ctx* ctx, float* z, float* cosv, float* sinv);
 

@@ -23,8 +23,8 @@ ZQ = 4096
 NANG = 256
 
 EXPORTS = ["glint_version", "glint_strerror", "glint_last_cuda_error", "glint_build_tables", "glint_create",
-           "glint_destroy", "glint_eval", "glint_eval_batch", "glint_eval_host", "glint_get_tables",
-           "glint_launch_count"]
+           "glint_destroy", "glint_eval", "glint_eval_batch", "glint_eval_host", "glint_eval_host_batch",
+           "glint_get_tables", "glint_launch_count"]
 
 
 class GlintError(RuntimeError):
@@ -97,6 +97,9 @@ def lib():
         L.glint_eval_host.argtypes = [C.c_void_p, C.POINTER(glint_gbuffer), C.POINTER(glint_scene), C.c_void_p,
                                       C.c_int64, C.c_void_p]
         L.glint_eval_host.restype = C.c_int
+        L.glint_eval_host_batch.argtypes = [C.c_void_p, C.c_int, C.POINTER(glint_gbuffer), C.POINTER(glint_scene),
+                                            C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_void_p]
+        L.glint_eval_host_batch.restype = C.c_int
         L.glint_get_tables.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.glint_get_tables.restype = C.c_int
         L.glint_launch_count.argtypes = [C.c_void_p]
@@ -284,3 +287,29 @@ def glint_eval_host(ctx: Context, gb, scene, out=None, stream=None):
     if rc:
         raise GlintError(rc, "glint_eval_host")
     return out
+
+
+def glint_eval_host_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
+    """End-to-end over several frames: host (ideally pinned) G-buffers in,
+    host radiance out, one continuous copy/compute pipeline across the frames.
+    Frame f equals glint_eval_host(ctx, gbs[f], scenes[f]) bit for bit.
+    Synchronous; returns the list of (H, W, 4) host tensors."""
+    import torch
+    n = len(gbs)
+    if len(scenes) != n or (outs is not None and len(outs) != n):
+        raise ValueError("gbs, scenes and outs must have the same length")
+    if n == 0:
+        return []
+    if any(g.planes()[0].device.type != "cpu" for g in gbs):
+        raise ValueError("glint_eval_host_batch needs host tensors")
+    G = (glint_gbuffer * n)(*[_gbuffer_struct(g) for g in gbs])
+    S = (glint_scene * n)(*[scene_struct(sc) for sc in scenes])
+    if outs is None:
+        outs = [torch.empty((G[f].height, G[f].width, 4), dtype=torch.float32).pin_memory() for f in range(n)]
+    P = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
+    Q = (C.c_int64 * n)(*[o.stride(0) // 4 for o in outs])
+    s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
+    rc = lib().glint_eval_host_batch(ctx.handle, n, G, S, P, Q, C.c_void_p(s.cuda_stream))
+    if rc:
+        raise GlintError(rc, "glint_eval_host_batch")
+    return outs

@@ -298,11 +298,10 @@ Range plane_range(const void* p, int64_t pitch, int w, int h) {
 bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi; }
 }  // namespace
 
-extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
-                                void* const* outs, const int64_t* out_pitches, void* stream) {
-  if (!c || n_frames < 0) return GLINT_EINVAL;
-  if (n_frames == 0) return GLINT_OK;
-  if (!gbs || !scenes || !outs || !out_pitches) return GLINT_EINVAL;
+// every frame valid; no output overlaps any input plane or another output
+// (frames of a batch run concurrently); the outputs non-null and aligned
+static int validate_batch(int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes, void* const* outs,
+                          const int64_t* out_pitches) {
   std::vector<Range> outr, inr;
   for (int f = 0; f < n_frames; ++f) {
     int rc = validate_scene(&scenes[f]);
@@ -322,6 +321,16 @@ extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gb
     for (size_t b = a + 1; b < outr.size(); ++b)
       if (overlap(outr[a], outr[b])) return GLINT_EALIAS;
   }
+  return GLINT_OK;
+}
+
+extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
+                                void* const* outs, const int64_t* out_pitches, void* stream) {
+  if (!c || n_frames < 0) return GLINT_EINVAL;
+  if (n_frames == 0) return GLINT_OK;
+  if (!gbs || !scenes || !outs || !out_pitches) return GLINT_EINVAL;
+  int rc = validate_batch(n_frames, gbs, scenes, outs, out_pitches);
+  if (rc) return rc;
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
@@ -360,6 +369,69 @@ static int ensure_stage(glint_ctx* c, size_t px) {
   return GLINT_OK;
 }
 
+// One continuous chunk stream over n frames: H2D of the next chunk (of this
+// or the next frame) overlaps the kernel and D2H of the previous one, so the
+// pipeline fills and drains once per call, not once per frame.
+static int host_pipeline(glint_ctx* c, int n, const glint_gbuffer* gbs, const glint_scene* scs, void* const* outs,
+                         const int64_t* out_pitches, void* stream) {
+  // GLINT_HOST_CHUNK_PX pixels per chunk (default 1M: 80 MB in, 16 MB out), at
+  // least 1 row. Measured on C2: 1M reaches 96.5 % of the pinned H2D bandwidth;
+  // 256K / 128K chunks lose more to per-chunk copies and launches (91 / 89 %)
+  // than they gain from the shorter non-overlapped tail
+#ifndef GLINT_HOST_CHUNK_PX
+#define GLINT_HOST_CHUNK_PX (1 << 20)
+#endif
+  size_t stage_px = 0;
+  for (int f = 0; f < n; ++f) {
+    const glint_gbuffer& g = gbs[f];
+    if (g.width == 0 || g.height == 0) continue;
+    int rows = (int)(GLINT_HOST_CHUNK_PX / g.width);
+    rows = rows < 1 ? 1 : (rows > g.height ? g.height : rows);
+    const size_t px = (size_t)rows * g.width;
+    stage_px = px > stage_px ? px : stage_px;
+  }
+  if (stage_px == 0) return GLINT_OK;
+  int rc = ensure_stage(c, stage_px);
+  if (rc) return rc;
+  GL_CUDA(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
+  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamWaitEvent(c->st[b], c->ev_in, 0));
+  int chunk = 0;
+  for (int f = 0; f < n; ++f) {
+    const glint_gbuffer* gb = &gbs[f];
+    const int W = gb->width, H = gb->height;
+    if (W == 0 || H == 0) continue;
+    int rows = (int)(GLINT_HOST_CHUNK_PX / W);
+    rows = rows < 1 ? 1 : (rows > H ? H : rows);
+    const void* planes[5] = {gb->duv, gb->uvm, gb->nrm, gb->pos, gb->mat};
+    const size_t rowb = (size_t)W * sizeof(float4);
+    for (int y0 = 0; y0 < H; y0 += rows, ++chunk) {
+      const int b = chunk & 1;
+      const int nr = (y0 + rows <= H) ? rows : H - y0;
+      cudaStream_t s = c->st[b];
+      for (int p = 0; p < 5; ++p)
+        GL_CUDA(cudaMemcpy2DAsync(c->d_stage[b][p], rowb, (const float4*)planes[p] + (int64_t)y0 * gb->pitch,
+                                  (size_t)gb->pitch * sizeof(float4), rowb, nr, cudaMemcpyHostToDevice, s));
+      glint_gbuffer sub;
+      sub.duv = c->d_stage[b][0];
+      sub.uvm = c->d_stage[b][1];
+      sub.nrm = c->d_stage[b][2];
+      sub.pos = c->d_stage[b][3];
+      sub.mat = c->d_stage[b][4];
+      sub.width = W;
+      sub.height = nr;
+      sub.pitch = W;
+      glint::KParams k = make_params(c, &sub, &scs[f], c->d_stage[b][5], W, nullptr);
+      GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
+      c->launches++;
+      GL_CUDA(cudaMemcpy2DAsync((float4*)outs[f] + (int64_t)y0 * out_pitches[f],
+                                (size_t)out_pitches[f] * sizeof(float4), c->d_stage[b][5], rowb, rowb, nr,
+                                cudaMemcpyDeviceToHost, s));
+    }
+  }
+  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamSynchronize(c->st[b]));
+  return GLINT_OK;
+}
+
 extern "C" int glint_eval_host(glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out_host,
                                int64_t out_pitch, void* stream) {
   if (!c) return GLINT_EINVAL;
@@ -373,46 +445,20 @@ extern "C" int glint_eval_host(glint_ctx* c, const glint_gbuffer* gb, const glin
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
   std::lock_guard<std::mutex> lock(c->host_mu);
-  const int W = gb->width, H = gb->height;
-  // GLINT_HOST_CHUNK_PX pixels per chunk (default 1M: 80 MB in, 16 MB out), at
-  // least 1 row. Measured on C2: 1M reaches 96.5 % of the pinned H2D bandwidth;
-  // 256K / 128K chunks lose more to per-chunk copies and launches (91 / 89 %)
-  // than they gain from the shorter non-overlapped tail
-#ifndef GLINT_HOST_CHUNK_PX
-#define GLINT_HOST_CHUNK_PX (1 << 20)
-#endif
-  int rows = (int)(GLINT_HOST_CHUNK_PX / W);
-  if (rows < 1) rows = 1;
-  if (rows > H) rows = H;
-  rc = ensure_stage(c, (size_t)rows * W);
+  void* outs[1] = {out_host};
+  return host_pipeline(c, 1, gb, sc, outs, &out_pitch, stream);
+}
+
+extern "C" int glint_eval_host_batch(glint_ctx* c, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
+                                     void* const* outs, const int64_t* out_pitches, void* stream) {
+  if (!c || n_frames < 0) return GLINT_EINVAL;
+  if (n_frames == 0) return GLINT_OK;
+  if (!gbs || !scenes || !outs || !out_pitches) return GLINT_EINVAL;
+  int rc = validate_batch(n_frames, gbs, scenes, outs, out_pitches);
   if (rc) return rc;
-  GL_CUDA(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
-  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamWaitEvent(c->st[b], c->ev_in, 0));
-  const void* planes[5] = {gb->duv, gb->uvm, gb->nrm, gb->pos, gb->mat};
-  const size_t rowb = (size_t)W * sizeof(float4);
-  int chunk = 0;
-  for (int y0 = 0; y0 < H; y0 += rows, ++chunk) {
-    const int b = chunk & 1;
-    const int nr = (y0 + rows <= H) ? rows : H - y0;
-    cudaStream_t s = c->st[b];
-    for (int p = 0; p < 5; ++p)
-      GL_CUDA(cudaMemcpy2DAsync(c->d_stage[b][p], rowb, (const float4*)planes[p] + (int64_t)y0 * gb->pitch,
-                                (size_t)gb->pitch * sizeof(float4), rowb, nr, cudaMemcpyHostToDevice, s));
-    glint_gbuffer sub;
-    sub.duv = c->d_stage[b][0];
-    sub.uvm = c->d_stage[b][1];
-    sub.nrm = c->d_stage[b][2];
-    sub.pos = c->d_stage[b][3];
-    sub.mat = c->d_stage[b][4];
-    sub.width = W;
-    sub.height = nr;
-    sub.pitch = W;
-    glint::KParams k = make_params(c, &sub, sc, c->d_stage[b][5], W, nullptr);
-    GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
-    c->launches++;
-    GL_CUDA(cudaMemcpy2DAsync((float4*)out_host + (int64_t)y0 * out_pitch, (size_t)out_pitch * sizeof(float4),
-                              c->d_stage[b][5], rowb, rowb, nr, cudaMemcpyDeviceToHost, s));
-  }
-  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamSynchronize(c->st[b]));
-  return GLINT_OK;
+  int cur = -1;
+  GL_CUDA(cudaGetDevice(&cur));
+  if (cur != c->device) return GLINT_EDEVICE;
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  return host_pipeline(c, n_frames, gbs, scenes, outs, out_pitches, stream);
 }

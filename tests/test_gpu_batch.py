@@ -194,3 +194,37 @@ def test_batches_on_concurrent_streams(ctx):
         torch.cuda.synchronize()
         for fr, o in list(zip(fa, oa)) + list(zip(fb, ob)):
             assert _same(o, refs[id(fr)])
+
+
+def test_host_batch_matches_per_frame_host_entry(ctx):
+    """glint_eval_host_batch (one copy/compute pipeline across frames) equals
+    glint_eval_host frame by frame, bit for bit: frames of different widths
+    (the chunk stage is sized for the largest), one larger than a 1M-pixel
+    chunk (several chunks per frame), a pitched host view, an empty frame."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    frs = [synth.c2(25), synth.c2(65, window=(300, 420, 0, 700)), synth.c2(45, window=(500, 501, 0, 1920))]
+    gbs = [fr.gbuf.pin() for fr in frs]
+    wide = synth.c2(85, window=(600, 664, 0, 400)).gbuf.pin()
+    gbs.append(synth.GBuffer(*[p[:, 30:330] for p in wide.planes()]))       # pitched host view
+    gbs.append(synth.GBuffer(*[p[:0] for p in wide.planes()]))              # empty
+    scs = [fr.scene for fr in frs] + [frs[0].scene, frs[0].scene]
+    outs = pkg.glint_eval_host_batch(ctx, gbs, scs)
+    assert outs[4].numel() == 0
+    for f in range(4):
+        ref = pkg.glint_eval_host(ctx, gbs[f], scs[f])
+        assert _same(outs[f], ref), f"frame {f}"
+    dev = pkg.glint_eval(ctx, gbs[0].to("cuda"), scs[0])
+    torch.cuda.synchronize()
+    assert _same(outs[0], dev.cpu())
+
+
+def test_host_batch_rejects_aliasing(ctx):
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    from paper_2306_05051_b200._lib import GLINT_EALIAS, GlintError
+    frs = [synth.c2(e, window=(500, 532, 0, 256)) for e in (15, 45)]
+    gbs = [fr.gbuf.pin() for fr in frs]
+    with pytest.raises(GlintError) as ei:
+        pkg.glint_eval_host_batch(ctx, gbs, [fr.scene for fr in frs], outs=[torch.empty(32, 256, 4), gbs[0].nrm])
+    assert ei.value.code == GLINT_EALIAS
