@@ -78,6 +78,14 @@ def test_batch_full_c2_step_bit_identical(ctx):
         torch.cuda.synchronize()
         for f, (o, r) in enumerate(zip(outs, refs)):
             assert _same(o, r), f"elevation frame {f}"
+    # the bench's launch configuration against the oracle directly: 800
+    # sampled pixels of every frame, recomputed one by one on the CPU
+    import oracle
+    g = torch.Generator().manual_seed(7)
+    for f, (fr, o) in enumerate(zip(frames, outs)):
+        idx = torch.randint(0, fr.gbuf.height * fr.gbuf.width, (800,), generator=g)
+        rgb_o, fl_o, _ = oracle.eval(fr.gbuf.take(idx).to("cpu"), fr.scene)
+        compare_radiance(o.reshape(-1, 4)[idx.to(o.device)], rgb_o, fl_o, f"batch C2 frame {f}")
 
 
 def test_batch_completion_is_ordered_before_later_stream_work(ctx):
