@@ -33,6 +33,15 @@ def main(path):
         _, rec = pkg.glint_eval(ctx, gd, fr.scene, debug=True)
         res[f"{name}_count"] = np.ascontiguousarray(rec["count"])
         res[f"{name}_host"] = pkg.glint_eval_host(ctx, fr.gbuf.pin(), fr.scene).numpy()
+    # the batch entries: all cases chained in one glint_eval_batch (PDL
+    # launches), and through one glint_eval_host_batch pipeline
+    frs = cases()
+    outs = pkg.glint_eval_batch(ctx, [fr.gbuf.to("cuda") for _, fr in frs], [fr.scene for _, fr in frs])
+    for (name, _), o in zip(frs, outs):
+        res[f"{name}_batch"] = o.cpu().numpy()
+    houts = pkg.glint_eval_host_batch(ctx, [fr.gbuf.pin() for _, fr in frs], [fr.scene for _, fr in frs])
+    for (name, _), o in zip(frs, houts):
+        res[f"{name}_hostbatch"] = o.numpy()
     torch.cuda.synchronize()
     ctx.close()
     np.savez(path, **res)

@@ -1,6 +1,7 @@
 """A checked build (-DGLINT_CHECKED: device asserts on every computed index,
 the stand-in for compute-sanitizer, which this pool does not offer) runs the
-TMA ring, pitched views, debug records, all eval modes and the host pipeline
+TMA ring, pitched views, debug records, all eval modes, the host pipeline and
+the two batch entries (chained launches, cross-frame host pipeline)
 on representative inputs without tripping an assert, and gives exactly the
 production library's bits."""
 import os
