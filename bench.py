@@ -226,13 +226,25 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-def read_profile_traffic():
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if not os.path.exists(p):
+def read_profile_traffic(config="C2"):
+    """The committed ncu evidence for this config: whole-step counts over every
+    frame of a step (profiles/ncu_counts_<config>.json, tools/ncu_step_counts.py:
+    SASS thread-instructions and DRAM bytes per pixel, averaged over the step's
+    frames, whose cost varies) and, for C2, the full capture of one frame
+    (profiles/ncu_summary.json: FP32 op counts). Returns (DRAM bytes per pixel,
+    counts dict with 'full' = the full-capture dict or None)."""
+    def load(name):
+        p = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(p):
+            return None
+        with open(p) as f:
+            return json.load(f)
+    counts = load(f"ncu_counts_{config.lower()}.json")
+    full = load("ncu_summary.json") if config == "C2" else None
+    if counts is None:
         return None, None
-    with open(p) as f:
-        d = json.load(f)
-    return d.get("dram_bytes_per_launch_per_pixel"), d
+    counts["full"] = full
+    return counts.get("dram_bytes_per_launch_per_pixel"), counts
 
 
 def measure_h2d_gbs(dev, nbytes=1 << 29, reps=3) -> float:
@@ -347,7 +359,7 @@ def run_ours(args):
     mean_launch_s = ms / 1e3 / launches
     evals_per_launch = evals / len(frames)
     achieved = evals_per_launch * w_eval / mean_launch_s
-    traffic_pp, prof = read_profile_traffic()
+    traffic_pp, prof = read_profile_traffic(args.config)
     px_per_launch = tot_px / len(frames)
     roofline = {
         "bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "thread-inst/s",
@@ -363,17 +375,20 @@ def run_ours(args):
         "serial_median_launch_ms": float(np.median(serial_launch_ms)),
         "serial_min_launch_ms": float(np.min(serial_launch_ms)),
     }
-    # the committed ncu capture is one C2 frame of the method (48 draws): its
-    # per-pixel SASS count applies to that workload only
-    if prof and prof.get("sass_thread_inst_per_pixel") and args.config == "C2" and args.draws == 48 \
-            and args.method == "ours":
-        # issue utilisation from the measured SASS count of the last ncu capture
+    # the committed ncu evidence is per config, for the method (48 draws):
+    # its per-pixel SASS count applies to that workload only
+    if prof and prof.get("sass_thread_inst_per_pixel") and args.draws == 48 and args.method == "ours":
+        # issue utilisation from the measured SASS count averaged over the step
         roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
         roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
-        roofline["traffic_source"] = f"profiles/ncu_summary.json ({prof.get('source')})"
-        if prof.get("fp32_flop_per_pixel"):
-            # FP32 arithmetic vs 2 x 128 x SMs x f (not the bound: ALU/issue is)
-            fl = px_per_launch * prof["fp32_flop_per_pixel"] / mean_launch_s
+        roofline["traffic_source"] = (f"profiles/ncu_counts_{args.config.lower()}.json ({prof.get('source')}, "
+                                      f"{prof.get('launches')} launches: every frame of a step)")
+        full = prof.get("full")
+        if full and full.get("fp32_flop_per_pixel") and full.get("sass_thread_inst_per_pixel"):
+            # FP32 arithmetic vs 2 x 128 x SMs x f (not the bound: ALU/issue is);
+            # the full capture's FP32 share of its frame's instructions, applied to the step's count
+            fl_pp = full["fp32_flop_per_pixel"] * prof["sass_thread_inst_per_pixel"] / full["sass_thread_inst_per_pixel"]
+            fl = px_per_launch * fl_pp / mean_launch_s
             roofline["fp32_tflops"] = fl / 1e12
             roofline["fp32_frac"] = fl / (2 * sms * LANES_PER_SM * f_max)
     cs = clk.summary()
