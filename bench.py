@@ -381,6 +381,11 @@ def run_ours(args):
         # issue utilisation from the measured SASS count averaged over the step
         roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
         roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
+        if prof.get("warp_inst_per_pixel"):
+            # issue-slot utilisation proper (smsp__inst_executed / (4 x SMs x cycles)): a
+            # warp instruction takes one slot however many lanes are active or predicated on
+            roofline["warp_inst_per_pixel"] = prof["warp_inst_per_pixel"]
+            roofline["issue_frac_warp"] = px_per_launch * prof["warp_inst_per_pixel"] / mean_launch_s / (sms * 4 * f_max)
         roofline["traffic_source"] = (f"profiles/ncu_counts_{args.config.lower()}.json ({prof.get('source')}, "
                                       f"{prof.get('launches')} launches: every frame of a step)")
         full = prof.get("full")
