@@ -343,6 +343,7 @@ def run_ours(args):
         ms, launches, clk = timed()
     ms_max = D.max_over_ranks(ms, device=dev)
     evals_all = D.sum_over_ranks(evals * args.steps, device=dev)
+    launches_all = int(round(D.sum_over_ranks(float(launches), device=dev)))   # every rank's kernels
     value = evals_all / (ms_max / 1e3)
 
     # ---- roofline of the dominant (only) kernel: issue-bound ALU path
@@ -496,7 +497,7 @@ def run_ours(args):
                                            if args.gather == "p2p" else "gathered to rank 0 after the timed region"))
                                        if args.config == "C5" else f"frames x{world} ranks, no data-path collective"),
                        **({"gather": gather} if gather else {})},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all,
             "clocks": cs, "gpu": props.name,
         }
         print(json.dumps(line), flush=True)
