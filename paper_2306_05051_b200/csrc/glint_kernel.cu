@@ -7,12 +7,15 @@
 // grids, S7 the 48 gated draws (fully unrolled, hashes finished in
 // registers, quantiles from a shared-memory table), S8 blend, S9 radiance.
 //
-// Persistent grid: the block count is capped at (#SMs x resident blocks per
-// SM) and blocks stride over 256-pixel tiles, so the 18 KB of tables are staged
-// into shared memory once per resident block. For contiguous G-buffers the
-// next tile's 5 planes (20 KB) are streamed HBM -> shared memory by the TMA
-// bulk-copy engine (cp.async.bulk + mbarrier, double-buffered) while the
-// current tile is shaded, so the DRAM latency is off the critical path.
+// Persistent grid: one 512-thread block per SM (128 registers) claims
+// 1024-pixel tiles dynamically from a per-launch counter, so the 18 KB of
+// tables are staged into shared memory once per block. For contiguous
+// G-buffers each tile's 5 planes (80 KB) stream HBM -> shared memory by the
+// TMA bulk-copy engine (cp.async.bulk + mbarrier) into a 2-stage ring, issued
+// two tiles ahead by the last warp to finish a stage, so the DRAM latency is
+// off the critical path. Every grid triggers its programmatic dependents at
+// entry and waits for its predecessor before exiting (glint_eval_batch chains
+// a step's frames).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
