@@ -3,7 +3,7 @@
  *
  * Implements the per-pixel glinty-BRDF evaluation of arXiv 2306.05051
  * ("distributed binomial laws on anisotropic grids") for a structure-of-arrays
- * G-buffer on NVIDIA B200 (sm_100a). One call = one kernel launch that runs
+ * G-buffer on NVIDIA B200 (sm_100a). One frame = one kernel launch that runs
  * every step of the path for every (pixel, light):
  *
  *   S1 footprint from screen-space uv derivatives
@@ -26,8 +26,9 @@
  *  - Device pointers are CUDA device addresses on the context's device; the
  *    caller owns every buffer (typically torch tensors). The library never
  *    allocates or frees caller memory and never synchronises the stream in
- *    glint_eval (errors of asynchronous execution surface at the caller's
- *    next synchronisation).
+ *    glint_eval / glint_eval_batch (errors of asynchronous execution surface
+ *    at the caller's next synchronisation). The host-buffer entries
+ *    (glint_eval_host, glint_eval_host_batch) are synchronous.
  *  - cudaStream_t is passed as void* (NULL = legacy default stream).
  */
 #ifndef GLINT_H
@@ -49,7 +50,8 @@ extern "C" {
 #define GLINT_ELIMIT -4   /* width*height or pitch*height >= 2^31 pixels */
 #define GLINT_ECUDA -5    /* a CUDA runtime call failed; see glint_last_cuda_error() */
 #define GLINT_ENOMEM -6   /* host or device allocation failed */
-#define GLINT_EALIAS -7   /* glint_eval_batch: an output overlaps an input plane or another output */
+#define GLINT_EALIAS -7   /* glint_eval_batch / glint_eval_host_batch: an output overlaps an input plane or
+                             another output */
 
 /* per-pixel output flags, stored as the bit pattern of out[pixel].w */
 #define GLINT_FLAG_INVALID 1u        /* meta bit0 clear: pixel not shaded */
