@@ -72,4 +72,8 @@ def test_our_arm_json_line_on_the_gpu():
     assert e["h2d_bytes_per_step"] == d["config"]["pixels_per_step"] * 80
     assert e["d2h_bytes_per_step"] == d["config"]["pixels_per_step"] * 16
     c = d["clocks"]
-    assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0 and isinstance(c["reasons"], list)
+    assert isinstance(c["reasons"], list) and "samples" in c
+    if c["samples"]:      # a 3-step region is short: NVML may not have sampled it
+        assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0
+    else:
+        assert c["reasons"] == ["nvml_unavailable"]
