@@ -1,8 +1,9 @@
 """Summarise an ncu --set full capture (+ optional launch list) into profiles/.
 
-usage: python tools/make_profiles.py <report.ncu-rep> <tag> [launches.csv]
-writes profiles/ncu_summary.json (read by bench.py for roofline.traffic and the
-SASS instruction count) and profiles/<tag>_ncu.md (human summary)."""
+usage: python tools/make_profiles.py <report.ncu-rep> <tag> [launches.csv] [--pix N --json PATH --launch TEXT]
+writes profiles/ncu_summary.json (the C2 frame's full capture; bench.py reads
+its FP32 op counts) or --json PATH for another config's frame (--pix = its
+pixels), and profiles/<tag>_ncu.md (human summary)."""
 import csv
 import io
 import json
@@ -10,8 +11,15 @@ import os
 import subprocess
 import sys
 
-rep, tag = sys.argv[1], sys.argv[2]
-launches = sys.argv[3] if len(sys.argv) > 3 else None
+args = sys.argv[1:]
+opts = {}
+for k in ("--pix", "--json", "--launch"):
+    if k in args:
+        i = args.index(k)
+        opts[k] = args[i + 1]
+        del args[i:i + 2]
+rep, tag = args[0], args[1]
+launches = args[2] if len(args) > 2 else None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, u, v = rows[0], rows[1], rows[2]
@@ -32,13 +40,16 @@ def to_bytes(k):
     return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(s, 1) if x is not None else None
 
 
-PIX = 1920 * 1080   # the captured launch is one C2 frame (bench --steps 1 --warmup 3, -s 3 -c 1)
+PIX = int(opts.get("--pix", 1920 * 1080))   # default: one C2 frame (bench --steps 1 --warmup 3, -s 3 -c 1)
+OUT_JSON = opts.get("--json", "profiles/ncu_summary.json")
+LAUNCH = opts.get("--launch", "one C2 1920x1080 frame (elevation 35 deg), bench.py --steps 1 --warmup 3")
 rd, wr = to_bytes("dram__bytes_read.sum"), to_bytes("dram__bytes_write.sum")
 tinst = f("sass__thread_inst_executed_true_per_opcode") or f("smsp__thread_inst_executed.sum")
-dur_ns = f("gpu__time_duration.sum") * {"nsecond": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6}.get(
+dur_ns = f("gpu__time_duration.sum") * {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6,
+                                         "second": 1e9, "s": 1e9}.get(
     units.get("gpu__time_duration.sum", "nsecond"), 1)
 summary = {
-    "source": os.path.basename(rep), "tag": tag, "launch": "one C2 1920x1080 frame (elevation 35 deg), bench.py --steps 1 --warmup 3",
+    "source": os.path.basename(rep), "tag": tag, "launch": LAUNCH,
     "pixels_per_launch": PIX,
     "gpu_time_us": dur_ns / 1e3,
     "sm_clock_ghz": f("sm__cycles_elapsed.avg.per_second"),
@@ -71,11 +82,11 @@ if None not in (ffma, fadd, fmul):
     summary["fp32_tflops"] = flop / (dur_ns * 1e-9) / 1e12
     summary["fp32_frac_of_peak_at_clock"] = flop / (dur_ns * 1e-9) / (2 * 128 * sms * clk)
 os.makedirs("profiles", exist_ok=True)
-with open("profiles/ncu_summary.json", "w") as fh:
+with open(OUT_JSON, "w") as fh:
     json.dump(summary, fh, indent=1)
 lines = [f"# ncu summary `{tag}` ({os.path.basename(rep)})", "",
          "Captured with `ncu --set full --clock-control none --import-source on -k regex:glint_eval_kernel -s 3 -c 1`",
-         "on `python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline` (one C2 1920x1080 frame).", "",
+         f"on {LAUNCH}.", "",
          "| metric | value |", "|---|---|"]
 for k, val in summary.items():
     if k != "stalls_per_issue":
