@@ -236,3 +236,39 @@ def test_host_batch_rejects_aliasing(ctx):
     with pytest.raises(GlintError) as ei:
         pkg.glint_eval_host_batch(ctx, gbs, [fr.scene for fr in frs], outs=[torch.empty(32, 256, 4), gbs[0].nrm])
     assert ei.value.code == GLINT_EALIAS
+
+
+def test_batches_write_pitched_outputs(ctx):
+    """Pitched outputs (out_pitch > width). The alias rule compares each
+    output's [first, last] byte span, so two frames written side by side as
+    column views of one wide buffer (interleaved rows, no common pixel) are
+    conservatively refused (documented in include/glint.h). Pitched views
+    into separate buffers are accepted, bit-identical to glint_eval, and the
+    padding columns stay untouched; device and host batch entries."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    from paper_2306_05051_b200._lib import GLINT_EALIAS, GlintError
+    frs = [synth.c2(e, window=(400, 464, 0, 300), device="cuda") for e in (25, 55)]
+    gbs, scs = [fr.gbuf for fr in frs], [fr.scene for fr in frs]
+    refs = [pkg.glint_eval(ctx, g, s) for g, s in zip(gbs, scs)]
+    wide = torch.full((64, 600, 4), 7.0, device="cuda")
+    # side-by-side column views: their address ranges interleave -> refused
+    with pytest.raises(GlintError) as ei:
+        pkg.glint_eval_batch(ctx, gbs, scs, outs=[wide[:, :300], wide[:, 300:]])
+    assert ei.value.code == GLINT_EALIAS
+    # pitched views into two separate wide buffers: accepted
+    w0 = torch.full((64, 400, 4), 7.0, device="cuda")
+    w1 = torch.full((64, 400, 4), 7.0, device="cuda")
+    outs = pkg.glint_eval_batch(ctx, gbs, scs, outs=[w0[:, 50:350], w1[:, 100:400]])
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert _same(o, r)
+    assert torch.all(w0[:, :50] == 7.0) and torch.all(w0[:, 350:] == 7.0) and torch.all(w1[:, :100] == 7.0)
+    # host entry with pitched host outputs
+    h0 = torch.full((64, 400, 4), 7.0).pin_memory()
+    h1 = torch.full((64, 400, 4), 7.0).pin_memory()
+    hin = [fr.gbuf.to("cpu").pin() for fr in frs]
+    houts = pkg.glint_eval_host_batch(ctx, hin, scs, outs=[h0[:, 50:350], h1[:, 100:400]])
+    for o, r in zip(houts, refs):
+        assert _same(o, r.cpu())
+    assert torch.all(h0[:, :50] == 7.0) and torch.all(h1[:, :100] == 7.0)
