@@ -186,9 +186,10 @@ int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene*
  * This is only correct because the frames do not depend on each other, so the
  * call checks it: every output range [outs[f], outs[f] + ((h-1)*out_pitch + w)
  * float4) must be disjoint from every input plane range of every frame and
- * from every other output, else GLINT_EALIAS (nothing launched). Ranges are
- * whole byte spans, so column views of one buffer that interleave row by row
- * count as overlapping (conservative: use separate buffers or row bands). Frame 0
+ * from every other output, else GLINT_EALIAS (nothing launched). The test is
+ * exact for regions of equal pitch (e.g. frames side by side as column views
+ * of one atlas are accepted) and conservative otherwise (overlapping
+ * [first, last] byte spans of regions with different pitches are refused). Frame 0
  * waits for all prior work on `stream` like glint_eval; work enqueued on
  * `stream` after the call sees every frame complete (each frame's grid waits
  * for its predecessor before it exits). Arguments: host arrays of n_frames

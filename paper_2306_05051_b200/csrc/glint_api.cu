@@ -290,12 +290,32 @@ extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const gli
 // dependent launch (frame f+1 fills the SMs frame f frees at its tail)
 // ---------------------------------------------------------------------------
 namespace {
-struct Range { uintptr_t lo, hi; };   // [lo, hi) bytes
+// a pitched region: h rows of w float4 at lo + r * pitch float4 (bytes below)
+struct Range { uintptr_t lo, hi; int64_t pitch, w, h; };   // [lo, hi): its whole span
 Range plane_range(const void* p, int64_t pitch, int w, int h) {
   const uintptr_t lo = (uintptr_t)p;
-  return {lo, lo + (uintptr_t)(((int64_t)(h - 1) * pitch + w) * 16)};
+  return {lo, lo + (uintptr_t)(((int64_t)(h - 1) * pitch + w) * 16), pitch * 16, (int64_t)w * 16, h};
 }
-bool overlap(Range a, Range b) { return a.lo < b.hi && b.lo < a.hi; }
+// do two regions share a byte? Disjoint spans: no. Equal pitches P: with
+// b.lo - a.lo = q P + rem (0 <= rem < P), b's row s starts at column rem of
+// a's row q + s and, if rem + b.w > P, runs on into a's row q + s + 1: exact
+// in O(1). Unequal pitches: the spans' overlap (conservative).
+bool overlap_one_way(const Range& a, const Range& b) {   // b.lo >= a.lo, same pitch (width <= pitch)
+  const int64_t P = a.pitch, d = (int64_t)(b.lo - a.lo);
+  const int64_t q = d / P, rem = d % P;
+  // rows of a that b's rows land on: q .. q + b.h - 1 (same column rem)
+  const bool same_row = rem < a.w && q < a.h;                 // b row 0 meets a row q (q >= 0)
+  const bool next_row = rem + b.w > P && q + 1 < a.h;          // b row 0 wraps into a row q + 1
+  return same_row || next_row;
+}
+bool overlap(Range a, Range b) {
+  if (!(a.lo < b.hi && b.lo < a.hi)) return false;
+  // a single row has no pitch of its own: it can take the other's if it fits
+  if (a.h == 1 && a.w <= b.pitch) a.pitch = b.pitch;
+  if (b.h == 1 && b.w <= a.pitch) b.pitch = a.pitch;
+  if (a.pitch != b.pitch) return true;
+  return a.lo <= b.lo ? overlap_one_way(a, b) : overlap_one_way(b, a);
+}
 }  // namespace
 
 // every frame valid; no output overlaps any input plane or another output

@@ -58,6 +58,9 @@ def test_scene_struct_layout(glib):
     assert C.sizeof(glib._lib.glint_gbuffer) == 5 * 8 + 4 + 4 + 8
 
 
+@pytest.mark.skipif(__import__("torch").cuda.is_available(),
+                    reason="fake, never dereferenced addresses are safe only where the device check fails "
+                           "(a passing call would dereference the fake context)")
 def test_batch_validation_and_alias_rules_without_gpu(glib):
     """glint_eval_batch validates every frame and the output/input overlap
     rule before it touches the context or the device (include/glint.h), so
@@ -105,3 +108,45 @@ def test_batch_validation_and_alias_rules_without_gpu(glib):
     assert L.glint_eval_batch(fake_ctx, 0, None, None, None, None, None) == m.GLINT_OK
     assert L.glint_eval_batch(None, 2, G, S, P, Q, None) == m.GLINT_EINVAL
     assert L.glint_eval_batch(fake_ctx, -1, G, S, P, Q, None) == m.GLINT_EINVAL
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(),
+                    reason="fake, never dereferenced addresses are safe only where the device check fails "
+                           "(a passing call would dereference the fake context)")
+def test_batch_alias_rule_against_brute_force(glib):
+    """The output-overlap rule of glint_eval_batch (include/glint.h) against a
+    brute-force pixel-set intersection over random pitched regions (fake,
+    never dereferenced addresses; no GPU): exact when the two regions share a
+    pitch (or one is a single row that fits the other's pitch), and never
+    missing a real overlap otherwise (conservative)."""
+    import random
+    import torch
+    L = glib.lib()
+    m = glib._lib
+    sc = m.scene_struct(__import__("paper_2306_05051_b200.synth", fromlist=["x"]).SceneParams())
+    S2 = (m.glint_scene * 2)(sc, sc)
+    fake = C.c_void_p(0x1000)
+    rng = random.Random(1)
+    for _ in range(6000):
+        P1, P2 = rng.choice([(8, 8), (8, 8), (6, 8), (8, 5)])
+        w1, h1, w2, h2 = rng.randint(1, P1), rng.randint(1, 5), rng.randint(1, P2), rng.randint(1, 5)
+        base = 0x100000
+        o1, o2 = base + 16 * rng.randint(0, 60), base + 16 * rng.randint(0, 60)
+        px1 = {o1 // 16 + r * P1 + c for r in range(h1) for c in range(w1)}
+        px2 = {o2 // 16 + r * P2 + c for r in range(h2) for c in range(w2)}
+        truth = bool(px1 & px2)
+        g0, g1 = m.glint_gbuffer(), m.glint_gbuffer()
+        g0.duv = g0.uvm = g0.nrm = g0.pos = g0.mat = 0x40000000
+        g1.duv = g1.uvm = g1.nrm = g1.pos = g1.mat = 0x50000000
+        g0.width, g0.height, g0.pitch = w1, h1, w1
+        g1.width, g1.height, g1.pitch = w2, h2, w2
+        G = (m.glint_gbuffer * 2)(g0, g1)
+        rc = L.glint_eval_batch(fake, 2, G, S2, (C.c_void_p * 2)(o1, o2), (C.c_int64 * 2)(P1, P2), None)
+        refused = rc == m.GLINT_EALIAS
+        if not torch.cuda.is_available():
+            assert refused or rc in (m.GLINT_ECUDA, m.GLINT_EDEVICE)
+        exact = P1 == P2 or (h1 == 1 and w1 <= P2) or (h2 == 1 and w2 <= P1)
+        if exact:
+            assert refused == truth, (P1, P2, w1, h1, w2, h2, o1 - base, o2 - base)
+        else:
+            assert refused or not truth, (P1, P2, w1, h1, w2, h2, o1 - base, o2 - base)

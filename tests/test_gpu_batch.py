@@ -239,12 +239,12 @@ def test_host_batch_rejects_aliasing(ctx):
 
 
 def test_batches_write_pitched_outputs(ctx):
-    """Pitched outputs (out_pitch > width). The alias rule compares each
-    output's [first, last] byte span, so two frames written side by side as
-    column views of one wide buffer (interleaved rows, no common pixel) are
-    conservatively refused (documented in include/glint.h). Pitched views
-    into separate buffers are accepted, bit-identical to glint_eval, and the
-    padding columns stay untouched; device and host batch entries."""
+    """Pitched outputs (out_pitch > width): two frames written side by side
+    as column views of one wide buffer (interleaved rows, no common pixel)
+    are accepted (the alias rule is exact for equal pitches), overlapping
+    column views are refused, pitched views into separate buffers leave their
+    padding untouched; all bit-identical to glint_eval; device and host batch
+    entries."""
     import paper_2306_05051_b200 as pkg
     from paper_2306_05051_b200 import synth
     from paper_2306_05051_b200._lib import GLINT_EALIAS, GlintError
@@ -252,9 +252,13 @@ def test_batches_write_pitched_outputs(ctx):
     gbs, scs = [fr.gbuf for fr in frs], [fr.scene for fr in frs]
     refs = [pkg.glint_eval(ctx, g, s) for g, s in zip(gbs, scs)]
     wide = torch.full((64, 600, 4), 7.0, device="cuda")
-    # side-by-side column views: their address ranges interleave -> refused
+    # side-by-side column views of one buffer: disjoint pixels -> accepted
+    outs = pkg.glint_eval_batch(ctx, gbs, scs, outs=[wide[:, :300], wide[:, 300:]])
+    torch.cuda.synchronize()
+    assert _same(wide[:, :300], refs[0]) and _same(wide[:, 300:], refs[1])
+    # overlapping column views (columns 250..299 shared) -> refused
     with pytest.raises(GlintError) as ei:
-        pkg.glint_eval_batch(ctx, gbs, scs, outs=[wide[:, :300], wide[:, 300:]])
+        pkg.glint_eval_batch(ctx, gbs, scs, outs=[wide[:, :300], wide[:, 250:550]])
     assert ei.value.code == GLINT_EALIAS
     # pitched views into two separate wide buffers: accepted
     w0 = torch.full((64, 400, 4), 7.0, device="cuda")
