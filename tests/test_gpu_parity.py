@@ -212,6 +212,24 @@ def test_full_size_c4_sampled(ctx):
     compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "C4 full")
 
 
+def test_full_size_c3_sampled(ctx):
+    """BASELINE.json configs[2]: one full 3840x2160 C3 frame (32 spheres on a
+    plane, anisotropic GGX alpha_x != alpha_y per object, one light), through
+    glint_eval_batch as bench.py launches frames; 2000 sampled pixels
+    recomputed one by one by the oracle (radiance 1e-4, flags exact)."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c3(device="cuda")
+    out = pkg.glint_eval_batch(ctx, [fr.gbuf], [fr.scene])[0].reshape(-1, 4)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(3)
+    idx = torch.randint(0, 3840 * 2160, (2000,), generator=g)
+    sub = fr.gbuf.take(idx).to("cpu")
+    rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+    compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "C3 full", mask=well_conditioned(sub, fr.scene))
+
+
 def test_tables_on_device(ctx, orc):
     z, c, s = ctx.tables()
     assert np.array_equal(z, orc.ztable()) and np.array_equal(c, orc.costable()) and np.array_equal(s, orc.sintable())
