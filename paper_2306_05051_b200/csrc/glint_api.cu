@@ -320,8 +320,8 @@ bool overlap(Range a, Range b) {
 
 // every frame valid; no output overlaps any input plane or another output
 // (frames of a batch run concurrently); the outputs non-null and aligned
-static int validate_batch(int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes, void* const* outs,
-                          const int64_t* out_pitches) {
+static int validate_batch_impl(int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
+                               void* const* outs, const int64_t* out_pitches) {
   std::vector<Range> outr, inr;
   for (int f = 0; f < n_frames; ++f) {
     int rc = validate_scene(&scenes[f]);
@@ -342,6 +342,17 @@ static int validate_batch(int n_frames, const glint_gbuffer* gbs, const glint_sc
       if (overlap(outr[a], outr[b])) return GLINT_EALIAS;
   }
   return GLINT_OK;
+}
+
+// no exception crosses the ABI: an allocation failure of the range lists is
+// GLINT_ENOMEM
+static int validate_batch(int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes, void* const* outs,
+                          const int64_t* out_pitches) {
+  try {
+    return validate_batch_impl(n_frames, gbs, scenes, outs, out_pitches);
+  } catch (...) {
+    return GLINT_ENOMEM;
+  }
 }
 
 extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gbuffer* gbs, const glint_scene* scenes,
