@@ -491,6 +491,9 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": desc, "pixels_per_step": tot_px, "valid_pixels_per_step": valid_px,
                        "evals_per_step_per_rank": evals, "lights": L, "launches_per_step": len(frames),
+                       "launch_path": ("glint_eval (one launch per frame)" if args.no_batch else
+                                       "glint_eval_batch (one call per step; frames chained by programmatic "
+                                       "dependent launch)"),
                        "l2": f"inputs {tot_px * 80 / 1e9:.2f} GB per rank > 126 MB L2: no flush between steps",
                        "parallelism": ((f"64 frames sharded over {world} ranks (f = rank mod {world}); radiance "
                                         + ("stored by the kernels straight into rank 0's buffer (peer memory)"
