@@ -276,3 +276,23 @@ def test_batches_write_pitched_outputs(ctx):
     for o, r in zip(houts, refs):
         assert _same(o, r.cpu())
     assert torch.all(h0[:, :50] == 7.0) and torch.all(h1[:, :100] == 7.0)
+
+
+def test_host_batch_mixed_eval_modes(ctx):
+    """One host batch mixing the method (48 draws), its 64/160-draw ablations
+    and the Zirr-style baseline: each chunk's launch takes its own frame's
+    mode; every frame equals its glint_eval bit for bit."""
+    import copy
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    base = synth.c2(45, window=(400, 528, 0, 960))
+    frames = []
+    for draws, method in ((48, "ours"), (160, "ours"), (48, "zk"), (64, "ours"), (48, "ours")):
+        sc = copy.deepcopy(base.scene)
+        sc.draws, sc.method = draws, method
+        frames.append(sc)
+    hin = base.gbuf.pin()
+    outs = pkg.glint_eval_host_batch(ctx, [hin] * len(frames), frames)
+    dev = base.gbuf.to("cuda")
+    for sc, o in zip(frames, outs):
+        assert _same(o, pkg.glint_eval(ctx, dev, sc).cpu()), (sc.draws, sc.method)
