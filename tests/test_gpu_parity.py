@@ -230,6 +230,27 @@ def test_full_size_c3_sampled(ctx):
     compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "C3 full", mask=well_conditioned(sub, fr.scene))
 
 
+def test_full_size_table1_beckmann_sampled(ctx):
+    """The Table 1 analogue's workload (tools/gpu/table1.py):
+    a 1920x1080 plane at 25 deg with Beckmann alpha = 1.0 and N = 2^16,
+    through glint_eval_batch; 2000 sampled pixels vs the oracle."""
+    import oracle
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c2(25, 1920, 1080, ndf="beckmann", alpha=1.0, device="cuda")
+    fr.gbuf.mat[..., 0] = 1.0
+    fr.gbuf.mat[..., 1] = 1.0
+    fr.gbuf.mat[..., 2] = 2.0 ** 16
+    out = pkg.glint_eval_batch(ctx, [fr.gbuf], [fr.scene])[0].reshape(-1, 4)
+    torch.cuda.synchronize()
+    g = torch.Generator().manual_seed(5)
+    idx = torch.randint(0, 1920 * 1080, (2000,), generator=g)
+    sub = fr.gbuf.take(idx).to("cpu")
+    rgb_o, fl_o, _ = oracle.eval(sub, fr.scene)
+    compare_radiance(out[idx.to("cuda")], rgb_o, fl_o, "Table 1 Beckmann", mask=well_conditioned(sub, fr.scene))
+    assert (rgb_o[:, 0] > 0).mean() > 0.01      # glints present in the sample
+
+
 def test_tables_on_device(ctx, orc):
     z, c, s = ctx.tables()
     assert np.array_equal(z, orc.ztable()) and np.array_equal(c, orc.costable()) and np.array_equal(s, orc.sintable())
