@@ -248,3 +248,38 @@ def test_contract_constants_are_the_fp32_closed_forms():
     assert float.fromhex("0x1.715476p+1") == f32(2 / math.log(2))
     assert float.fromhex("0x1.715476p+0") == f32(1 / math.log(2))
     assert "0x1.715476p+1f" in src
+
+
+def test_draw_hash_is_two_to_one_and_its_gate_bias_is_bounded(orc):
+    """The draw hash's xor-rotate (R-23b) is linear over GF(2) with kernel
+    {0, ~0}: t and ~t give the same word (t = x C1, so x and C1^-1 ~(x C1)
+    collide), every word it produces has even parity, so draw_hash takes 2^31
+    values, each from exactly 2 inputs. Under
+    a uniform input the gate (y >> 9) < T therefore has probability
+    2 |{y < 512 T : C2^-1 y has even parity}| / 2^32 instead of T / 2^23.
+    Pinned: the 2-to-1 structure on the oracle's own function, and the exact
+    relative bias: <= 6 % at T <= 8 (P(gate) ~ 1e-7, where the contract's
+    ceil(P 2^23) already errs by up to 1/T), <= 0.5 % for 16 <= T <= 8192,
+    and <= 0.1 % from T = 2^13 on (R-23b)."""
+    rng = np.random.default_rng(41)
+    c1, c1inv = 0x7feb352d, pow(0x7feb352d, -1, 2 ** 32)
+    for x in [int(v) for v in rng.integers(0, 2 ** 32, 200, dtype=np.uint64)] + [0, 1, 0x80000000]:
+        twin = ((~(x * c1) & 0xFFFFFFFF) * c1inv) & 0xFFFFFFFF     # x C1 and its complement
+        assert twin != x and orc.draw_hash(x) == orc.draw_hash(twin)
+    # even parity of the rotated word: t ^ rotr(t, 15) for t = x * C1
+    U, M = np.uint64, np.uint64(0xFFFFFFFF)
+    t = (rng.integers(0, 2 ** 32, 100000, dtype=np.uint64) * U(0x7feb352d)) & M
+    u = t ^ (((t >> U(15)) | (t << U(17))) & M)
+    par = np.array([bin(int(v)).count("1") & 1 for v in u[:2000]])
+    assert not par.any()
+    # exact gate probability for T up to 2^14 from the parity characterisation
+    inv = U(pow(0x846ca68b, -1, 2 ** 32))
+    y = np.arange(512 * 16384, dtype=np.uint64)
+    w = (y * inv) & M
+    for s in (16, 8, 4, 2, 1):
+        w ^= w >> U(s)
+    cs = np.cumsum(1 - (w & U(1)).astype(np.int64))
+    for T in (1, 2, 3, 4, 5, 8, 16, 32, 64, 100, 256, 1000, 1024, 4096, 8192, 16384):
+        rel = (2.0 * cs[512 * T - 1] / 2 ** 32) / (T / 2 ** 23) - 1.0
+        bound = 0.06 if T <= 8 else (0.005 if T < 8192 else 0.001)
+        assert abs(rel) <= bound, (T, rel)
