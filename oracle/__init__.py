@@ -113,6 +113,9 @@ def lib():
             L.orc_smith_g2.restype = C.c_double
             L.orc_schlick.argtypes = [C.c_double, C.c_double]
             L.orc_schlick.restype = C.c_double
+            L.orc_shell.argtypes = [C.POINTER(_Scene), C.c_int32, C.c_float * 3, C.c_float * 3, C.c_float, C.c_float,
+                                    C.c_double, d3]
+            L.orc_shell.restype = C.c_int
             f16 = C.c_float * 16
             L.orc_zk_probes.argtypes = [C.c_float * 4, C.c_float, C.c_float, f16, f16, fp, C.POINTER(C.c_uint32)]
             L.orc_zk_probes.restype = C.c_int
@@ -303,6 +306,17 @@ def smith_g2(ndf: str, ax, ay, wi_local, wo_local) -> float:
 
 def schlick(f0: float, cos_t: float) -> float:
     return lib().orc_schlick(f0, cos_t)
+
+
+def shell(scene, light: int, nrm, pos, ax: float, ay: float, Dp: float):
+    """The S9 radiance shell of one light (fp64): (rgb contribution, added?)
+    for a pixel with normal ``nrm``, position ``pos`` and D_P = ``Dp``."""
+    f3 = C.c_float * 3
+    rgb = (C.c_double * 3)()
+    sc = scene_struct(scene)
+    added = lib().orc_shell(C.byref(sc), light, f3(*[float(x) for x in nrm[:3]]), f3(*[float(x) for x in pos[:3]]),
+                            ax, ay, Dp, rgb)
+    return np.array(list(rgb)), bool(added)
 
 
 # --------------------------------------------------------------------------- ZK baseline pieces

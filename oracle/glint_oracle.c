@@ -191,13 +191,16 @@ uint32_t orc_lowbias32(uint32_t x) {
 
 /* the per-draw hash h = draw_hash(hs + ka) of the spatial seed hs and the
  * angular seed ka (both full lowbias32 outputs): the last four steps of
- * lowbias32 with the middle xor-shift replaced by an xor-rotate by 15
- * (reading R-23b: the shift leaves chi-square-detectable dependence between the
- * 4 node draws of a texel, whose sums differ by fixed offsets; the rotation
- * feeds the top bits of x*C1 back into the low bits and removes it) */
+ * lowbias32 with the middle xor-shift replaced by a three-term xor-rotate
+ * x ^ rotr(x, 11) ^ rotr(x, 19) (reading R-23b). The shift leaves chi-square-
+ * detectable dependence between the 4 node draws of a texel, whose sums
+ * differ by fixed offsets; the rotations feed the top bits of x*C1 back into
+ * the low bits. An odd number of rotation terms makes the step invertible
+ * (1 + t^11 + t^19 is a unit modulo t^32 - 1 over GF(2)), so draw_hash is a
+ * bijection of 32-bit words and theta0 stays exactly uniform. */
 uint32_t orc_draw_hash(uint32_t x) {
   x *= 0x7feb352dU;
-  x ^= (x >> 15) | (x << 17);
+  x ^= ((x >> 11) | (x << 21)) ^ ((x >> 19) | (x << 13));
   x *= 0x846ca68bU;
   x ^= x >> 16;
   return x;
@@ -698,6 +701,53 @@ static double zk_blend(int npr, const float uk[16], const float vk[16], float A,
 }
 
 /* ---------------------------------------------------------------------- */
+/* S9  Radiance shell of one light (Eq. 1-2: L = F G D_P E / (4
+ * n.wi) for a punctual light; readings R-21, R-27). Everything in
+ * fp64 from the raw fp32 inputs (normal, position, view, light): no fp32
+ * rounding of a cosine reaches the radiance. Called for a light the fp32
+ * decision path found active; adds nothing when D_P = 0 (no flake reflects)
+ * or when an fp64 cosine n.wi, n.wo is not > 0 (the exact geometry is at or
+ * below the horizon although the fp32 decision said otherwise). Adds the
+ * light's RGB contribution to rgb; returns 1 if it added anything.         */
+/* ---------------------------------------------------------------------- */
+int orc_shell(const orc_scene* sc, int32_t l, const float nrm[3], const float pos[3], float ax, float ay,
+              double Dp, double rgb[3]) {
+  if (!(Dp > 0.0)) return 0;
+  const orc_light* lt = &sc->lights[l];
+  double nd[3] = {nrm[0], nrm[1], nrm[2]};
+  normalize3d(nd);
+  double td[3], bd[3];
+  onb_d(nd, td, bd);
+  double wid[3];  /* towards the viewer: pinhole camera (R-27) or direction */
+  if (sc->view_kind == 0) { wid[0] = (double)sc->view[0] - pos[0]; wid[1] = (double)sc->view[1] - pos[1]; wid[2] = (double)sc->view[2] - pos[2]; }
+  else { wid[0] = sc->view[0]; wid[1] = sc->view[1]; wid[2] = sc->view[2]; }
+  normalize3d(wid);
+  double wod[3], E[3];  /* towards the light; irradiance E = I / d^2 (point) or I */
+  if (lt->kind == 0) {
+    wod[0] = (double)lt->pos_or_dir[0] - pos[0]; wod[1] = (double)lt->pos_or_dir[1] - pos[1]; wod[2] = (double)lt->pos_or_dir[2] - pos[2];
+    double d2 = dot3d(wod, wod);
+    for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch] / d2;
+  } else {
+    wod[0] = lt->pos_or_dir[0]; wod[1] = lt->pos_or_dir[1]; wod[2] = lt->pos_or_dir[2];
+    for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch];
+  }
+  normalize3d(wod);
+  double nid = dot3d(nd, wid), nod = dot3d(nd, wod);
+  if (!(nid > 0.0) || !(nod > 0.0)) return 0;
+  double hd[3] = {wid[0] + wod[0], wid[1] + wod[1], wid[2] + wod[2]};
+  normalize3d(hd);
+  double cih = dot3d(wid, hd);
+  double wil[3] = {dot3d(wid, td), dot3d(wid, bd), nid};
+  double wol[3] = {dot3d(wod, td), dot3d(wod, bd), nod};
+  double G2 = orc_smith_g2(sc->ndf_kind, ax, ay, wil, wol);
+  for (int ch = 0; ch < 3; ++ch) {
+    double F = orc_schlick((double)sc->f0[ch], cih);
+    rgb[ch] += F * G2 * Dp * E[ch] / (4.0 * nid);
+  }
+  return 1;
+}
+
+/* ---------------------------------------------------------------------- */
 /* S0..S9 for one pixel                                                     */
 /* ---------------------------------------------------------------------- */
 static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4],
@@ -792,16 +842,6 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
   float ni = dot3f(nf, wi);
   float inv_beta = 1.0f / sc->beta;
 
-  /* fp64 frame for radiance */
-  double nd[3] = {nrm[0], nrm[1], nrm[2]};
-  normalize3d(nd);
-  double td[3], bd[3];
-  onb_d(nd, td, bd);
-  double wid[3];
-  if (sc->view_kind == 0) { wid[0] = (double)sc->view[0] - pos[0]; wid[1] = (double)sc->view[1] - pos[1]; wid[2] = (double)sc->view[2] - pos[2]; }
-  else { wid[0] = sc->view[0]; wid[1] = sc->view[1]; wid[2] = sc->view[2]; }
-  normalize3d(wid);
-
   for (int l = 0; l < L; ++l) {
     const orc_light* lt = &sc->lights[l];
     orc_rec* rc = rec ? &rec[l] : 0;
@@ -864,34 +904,11 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       C += Ci; /* distributed law: sum over the grids (Eq. 10/13) */
     }
 
-    /* S8: Eq. 3-4, D_P = D(n)/R * b / N(P), N(P) = N P (reading R-20) */
-    double Dn = 1.0 / (M_PI * (double)ax * (double)ay);
-    /* no flake reflects (C = 0, e.g. N = 0 or p = 0): D_P = 0, not 0/0 */
-    double Dp = C > 0.0 ? Dn * C / ((double)R * (double)N * (double)P) : 0.0;
-
-    /* S9: Eq. 1-2 with a punctual light: L += F G D_P E / (4 n.wi) */
-    double wod[3];
-    double E[3];
-    if (lt->kind == 0) {
-      wod[0] = (double)lt->pos_or_dir[0] - pos[0]; wod[1] = (double)lt->pos_or_dir[1] - pos[1]; wod[2] = (double)lt->pos_or_dir[2] - pos[2];
-      double d2 = dot3d(wod, wod);
-      for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch] / d2;
-    } else {
-      wod[0] = lt->pos_or_dir[0]; wod[1] = lt->pos_or_dir[1]; wod[2] = lt->pos_or_dir[2];
-      for (int ch = 0; ch < 3; ++ch) E[ch] = (double)lt->intensity[ch];
-    }
-    normalize3d(wod);
-    double hd[3] = {wid[0] + wod[0], wid[1] + wod[1], wid[2] + wod[2]};
-    normalize3d(hd);
-    double nid = dot3d(nd, wid);
-    double cih = dot3d(wid, hd);
-    double wil[3] = {dot3d(wid, td), dot3d(wid, bd), nid};
-    double wol[3] = {dot3d(wod, td), dot3d(wod, bd), dot3d(wod, nd)};
-    double G2 = 1.0 / (1.0 + smith_lambda(sc->ndf_kind, ax, ay, wil) + smith_lambda(sc->ndf_kind, ax, ay, wol));
-    for (int ch = 0; ch < 3; ++ch) {
-      double F = orc_schlick((double)sc->f0[ch], cih);
-      rgb[ch] += F * G2 * Dp * E[ch] / (4.0 * nid);
-    }
+    /* S8: Eq. 3-4, D_P = D(n)/R * b / N(P), N(P) = N P (reading R-20); no
+     * flake reflects (C = 0, e.g. N = 0 or p = 0): D_P = 0, not 0/0 */
+    double Dp = C > 0.0 ? C / (M_PI * (double)ax * (double)ay * (double)R * (double)N * (double)P) : 0.0;
+    /* S9: Eq. 1-2, fp64 shell from the raw fp32 inputs */
+    orc_shell(sc, l, nrm, pos, ax, ay, Dp, rgb);
     if (rc) { rc->C = (float)C; rc->Dp = (float)Dp; }
   }
   *flags_out = flags;

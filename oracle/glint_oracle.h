@@ -104,6 +104,10 @@ float orc_gated_count(uint32_t h, uint32_t T, float sigma, float m1, float cap);
 float orc_ratio(int32_t ndf_kind, float ax, float ay, float hx, float hy, float hz);
 double orc_smith_g2(int32_t kind, double ax, double ay, const double wi_l[3], const double wo_l[3]);
 double orc_schlick(double f0, double cos_t);
+/* S9 shell of light l (fp64 from the raw fp32 inputs): adds F G2 Dp E / (4 n.wi)
+ * to rgb when Dp > 0 and both fp64 cosines are > 0; returns 1 if it added. */
+int orc_shell(const orc_scene* sc, int32_t l, const float nrm[3], const float pos[3], float ax, float ay,
+              double Dp, double rgb[3]);
 int orc_zk_probes(const float duv[4], float u, float v, float uk[16], float vk[16], float* area,
                   uint32_t* flags);
 void orc_zk_lod(float A, int32_t* kz, float* t);

@@ -52,8 +52,20 @@ def tail3(x, rotate=False):       # t = x*C1; u = t ^ t>>15 (or rotr 15); y = u*
     return (u * C2) & M, u
 
 
+def rotr(t, k):
+    return ((t >> U(k)) | (t << U(32 - k))) & M
+
+
 def cand(name, hs, ka):
     """-> (y: gate word (bits 9..31), q: quantile index 0..4095)."""
+    if name.startswith("rot3"):          # rot3:a:b -- t = x*C1; u = t ^ rotr(t,a) ^ rotr(t,b); y = u*C2 (bijective)
+        _, a, b = name.split(":")[:3]
+        t = ((hs + ka) & M) * C1 & M
+        u = t ^ rotr(t, int(a)) ^ rotr(t, int(b))
+        y = (u * C2) & M
+        if name.endswith(":u"):          # quantile index from u (one op fewer)
+            return y, (u >> U(2)) & U(4095)
+        return y, ((y ^ (y >> U(16))) >> U(2)) & U(4095)
     if name == "current":
         y, _ = tail3(hs + ka, rotate=True)
         return y, ((y ^ (y >> U(16))) >> U(2)) & U(4095)
@@ -76,7 +88,7 @@ def cand(name, hs, ka):
     raise ValueError(name)
 
 
-OPS = {"current": 5, "shift15": 5, "xor_mul": 2, "premix": 7, "xor_tail": 6, "u_index": 4}
+OPS = {"rot3:15:7": 6, "current": 5, "shift15": 5, "xor_mul": 2, "premix": 7, "xor_tail": 6, "u_index": 4}
 
 
 def battery(name, n, cells, seed=0):
@@ -102,7 +114,7 @@ def battery(name, n, cells, seed=0):
                 gb = ((ys[b] >> U(9)) < U(1 << 21)).astype(float)
                 corr_g.append(abs(np.corrcoef(ga, gb)[0, 1]))
                 corr_q.append(abs(np.corrcoef(z[qs[a].astype(np.int64)], z[qs[b].astype(np.int64)])[0, 1]))
-    return dict(ops=OPS[name], worst_chi2_p=worst_p, max_corr_gate=float(max(corr_g)),
+    return dict(ops=OPS.get(name, 6 if not name.endswith(':u') else 5), worst_chi2_p=worst_p, max_corr_gate=float(max(corr_g)),
                 max_corr_quantile=float(max(corr_q)), pairs=len(corr_g))
 
 
@@ -138,13 +150,14 @@ def main():
     ap.add_argument("--cells", type=int, default=24)
     ap.add_argument("--node-pairs", type=int, default=0)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--names", default=None, help="comma-separated candidates (e.g. rot3:15:7,rot3:13:21:u)")
     a = ap.parse_args()
     if a.node_pairs:
-        for name in ("current", "premix"):
+        for name in (a.names.split(",") if a.names else ("current", "premix")):
             print(name, node_pair_scan(name, a.node_pairs), flush=True)
         return
     res = {}
-    for name in OPS:
+    for name in (a.names.split(",") if a.names else OPS):
         res[name] = battery(name, a.n, a.cells)
         r = res[name]
         print(f"{name:9s} ops {r['ops']}  max|corr| gate {r['max_corr_gate']:.4f} quantile {r['max_corr_quantile']:.4f}  "
