@@ -1,27 +1,36 @@
 #!/usr/bin/env python
 """Benchmark of the glint hot path (BASELINE.json metric: glint shading
-evals/s, one eval = one valid pixel x one light = 48 gated binomial draws).
+evals/s, one eval = one ACTIVE (pixel, light) pair -- a valid pixel with a
+non-degenerate footprint and the light above its horizon, the pairs whose
+48 gated binomial draws the kernel performs; counted by glint_count_active).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C5|C2|C3|C4] [--gather p2p|nccl]
 
 One step = one pass of the whole hot path (S0-S9) over one
-batch of synthetic input: for C2 (default, BASELINE.json configs[1]) the
-10-elevation set of 1920x1080 ground-plane frames, one point light. Inputs
-are resident in HBM when the timed region starts; they total 1.66 GB per
-rank (> 126 MB L2), so no L2 flush is needed between steps. For N > 1
-(torchrun) every rank shades its own frame set (hash seed differs per rank),
-no data-path collective: weak scaling, value = evals of all ranks / max-over-
-ranks device time.
+batch of synthetic input. Default workload: C5 (BASELINE.json configs[4]),
+the 64-frame 3840x2160 zoom path with 4 point lights, at every N (strong
+scaling: the same 64 frames whatever the GPU count). Frames are dealt round-
+robin to ranks (frame f on rank f mod N); C2 / C3 at N > 1 deal 64-row bands
+instead. The gather of radiance to rank 0 is INSIDE the timed
+region: by default fused into the kernels (each rank stores its tiles straight
+into rank 0's full-frame buffers over NVLink, CUDA IPC), or with --gather nccl
+as per-tile send/recv rounds on a communication stream overlapped with the
+next tiles' shading. Inputs are resident in HBM when the timed region starts
+and total > 126 MB L2 per rank (no flush needed).
 
+``--gpus N`` without torchrun re-launches itself through torch.distributed.run
+with N processes; a world size that differs from N prints no result line.
 Prints ONE JSON line on rank 0. ``--impl reference`` times the CPU oracle
-(oracle/) on the host cores over a bounded sample of the same workload.
+(oracle/) on the host cores over the same bounded sample our arm's
+cpu_baseline uses.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import sys
 import threading
 import time
@@ -40,7 +49,6 @@ UNIT = "evals/s"
 W_PIXEL, W_EVAL = 340.0, 1110.0
 # Algorithmic HBM bytes per pixel: 5 float4 planes in + 1 float4 out.
 BYTES_PER_PIXEL = 96.0
-SM_COUNT_B200 = 148
 LANES_PER_SM = 128
 
 
@@ -115,66 +123,83 @@ class ClockSampler:
         return False
 
 
-# ----------------------------------------------------------------------------- workload
-C5_FRAMES = 64
-C5_DESC = ("C5: 64-frame 3840x2160 zoom path (distance 0.5 -> 500, elevation 30 deg) over the 32-sphere scene, "
-           "4 point lights, anisotropic GGX alpha U(0.05,0.6), N log-U[1e3,1e7]; frames sharded across ranks, "
-           "radiance gathered to rank 0")
-
-
-def make_frames(config: str, device, seed: int, rank: int = 0, world: int = 1):
+# ----------------------------------------------------------------------------- workloads
+def _gen(config):
     from paper_2306_05051_b200 import synth
-    if config == "C5":
-        # BASELINE.json configs[4]: the zoom path, frames sharded f = rank (mod world);
-        # one fixed image set whatever the GPU count (strong scaling)
-        from paper_2306_05051_b200 import dist as D
-        ids = D.shard(range(C5_FRAMES), rank, world)
-        frames = [synth.c5(f, device=device) for f in ids]
-        for fr, f in zip(frames, ids):
-            fr.frame_id = f
-        return frames, C5_DESC
-    if config == "C2":
-        frames = synth.c2_frames(device=device)
-        desc = ("C2: 1920x1080 infinite ground plane, pinhole 60deg FOV, elevations 5..85 + 90 deg "
-                "(10 frames per step), 1 point light, GGX alpha 0.2, N = 2^U(8,20) per uv tile, R = 0.034")
-    elif config == "C4":
-        frames = [synth.c4(f, device=device) for f in range(8)]
-        desc = ("C4: 3840x2160, 32 spheres on a plane, anisotropic GGX alpha U(0.05,0.6), N log-U[1e3,1e7], "
-                "16 point lights, 8 jittered frames per step")
-    else:
-        raise SystemExit(f"unknown config {config}")
-    for fr in frames:
-        fr.scene.seed = seed
-    return frames, desc
+    return {
+        "C2": lambda f, win, dev: synth.c2(synth.C2_ELEVATIONS[f], window=win, device=dev),
+        "C3": lambda f, win, dev: synth.c3(window=win, device=dev),
+        "C4": lambda f, win, dev: synth.c4(f, window=win, device=dev),
+        "C5": lambda f, win, dev: synth.c5(f, window=win, device=dev),
+    }[config]
 
 
-def count_evals(frames):
-    tot_px = sum(fr.gbuf.height * fr.gbuf.width for fr in frames)
-    evals = sum(fr.gbuf.valid_count() * len(fr.scene.lights) for fr in frames)
-    valid_px = sum(fr.gbuf.valid_count() for fr in frames)
-    return tot_px, valid_px, evals
+# (frames per step, height, width, description); BASELINE.json configs[1..4]
+WORKLOADS = {
+    "C2": (10, 1080, 1920, "C2: 1920x1080 infinite ground plane, pinhole 60deg FOV, elevations 5..85 + 90 deg "
+                           "(10 frames per step), 1 point light, GGX alpha 0.2, N = 2^U(8,20) per uv tile, R = 0.034"),
+    "C3": (1, 2160, 3840, "C3: 3840x2160, 32 analytic spheres on a plane, anisotropic GGX alpha U(0.05,0.6), "
+                          "N log-U[1e3,1e7], 1 point light (1 frame per step)"),
+    "C4": (8, 2160, 3840, "C4: 3840x2160, 32 spheres on a plane, anisotropic GGX alpha U(0.05,0.6), "
+                          "N log-U[1e3,1e7], 16 point lights, 8 jittered frames per step"),
+    "C5": (64, 2160, 3840, "C5: 64-frame 3840x2160 zoom path (distance 0.5 -> 500, elevation 30 deg) over the "
+                           "32-sphere scene, 4 point lights, anisotropic GGX alpha U(0.05,0.6), N log-U[1e3,1e7]"),
+}
+# the bounded CPU sample shared by cpu_baseline and --impl reference: 8-row
+# bands every `period` rows (centred), of the listed frames
+SAMPLE = {"C2": (range(10), 16), "C3": ((0,), 16), "C4": (range(8), 256), "C5": (range(0, 64, 4), 270)}
 
 
-# ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(frames, row_stride: int):
-    """Deterministic bounded sample of the workload: every ``row_stride``-th row
-    of every frame (all lights), as host arrays."""
+def oracle_sample(config: str):
+    """[(GBuffer on CPU, scene)] of the sample and its description."""
     from paper_2306_05051_b200 import synth
+    frames, period = SAMPLE[config]
+    _, H, W, _ = WORKLOADS[config]
+    gen = _gen(config)
     subs = []
-    for fr in frames:
-        gb = synth.GBuffer(*[p[::row_stride].contiguous().cpu() for p in fr.gbuf.planes()])
-        subs.append((gb, fr.scene))
-    return subs
+    for f in frames:
+        parts, sc = [], None
+        for y in range(period // 2 - 4, H, period):
+            fr = gen(f, (y, min(H, y + 8), 0, W), "cpu")
+            parts.append(fr.gbuf)
+            sc = fr.scene
+        subs.append((synth.GBuffer(*[torch.cat([p.planes()[k] for p in parts], 0) for k in range(5)]), sc))
+    nf = len(list(frames))
+    desc = f"8-row bands every {period} rows of {nf} frames of {config}" + (" (every 4th frame)" if config == "C5" else "")
+    return subs, desc
 
 
 def time_oracle(subs, threads=None):
+    """One pass of the oracle over the sample: (active evals, seconds)."""
     import oracle
     t0 = time.perf_counter()
     ev = 0
     for gb, sc in subs:
         oracle.eval(gb, sc, threads=threads)
-        ev += gb.valid_count() * len(sc.lights)
-    return ev, time.perf_counter() - t0
+    dt = time.perf_counter() - t0
+    for gb, sc in subs:
+        ev += _active_pairs_oracle(gb, sc)
+    return ev, dt
+
+
+_ACTIVE_CACHE = {}
+
+
+def _active_pairs_oracle(gb, sc):
+    """Active (pixel, light) pairs of a sample part, from the oracle's records
+    (light_active), computed once (outside any timing)."""
+    import oracle
+    key = (id(gb), id(sc))
+    if key not in _ACTIVE_CACHE:
+        n = 0
+        planes = gb.planes()
+        H = planes[0].shape[0]
+        for y in range(0, H, 8):           # bounded record memory (one 8-row band at a time)
+            sub = type(gb)(*[p[y:y + 8] for p in planes])
+            _, _, rec = oracle.eval(sub, sc, debug=True)
+            n += int(rec["light_active"].sum())
+        _ACTIVE_CACHE[key] = n
+    return _ACTIVE_CACHE[key]
 
 
 def host_cores():
@@ -186,20 +211,12 @@ def run_reference(args):
     rank, world, _ = D.env_rank_world()
     if rank != 0:
         return 0
-    if args.config == "C5":
-        # 64 full 4K frames on the CPU would take minutes to synthesise: the
-        # bounded sample is an 8-row band through the middle of every frame
-        from paper_2306_05051_b200 import synth
-        frames = [synth.c5(f, window=(1076, 1084, 0, 3840)) for f in range(C5_FRAMES)]
-        desc = C5_DESC
-        stride = 1
-    else:
-        frames, desc = make_frames(args.config, "cpu", seed=1)
-        stride = 64 if args.config == "C2" else 256
-    for fr in frames:
-        fr.scene.draws = args.draws
-        fr.scene.method = args.method
-    subs = oracle_sample(frames, stride)
+    _, _, _, desc = WORKLOADS[args.config]
+    subs, sample = oracle_sample(args.config)
+    for gb, sc in subs:
+        sc.draws = args.draws
+        sc.method = args.method
+        _active_pairs_oracle(gb, sc)
     cores = host_cores()
     for _ in range(args.warmup):
         time_oracle(subs)
@@ -209,14 +226,11 @@ def run_reference(args):
         ev_tot += ev
         t_tot += t
     value = ev_tot / t_tot
-    if args.config == "C5":
-        sample = f"rows 1076-1083 of each of the 64 frames of C5 ({ev_tot // args.steps} evals/step)"
-    else:
-        sample = f"every {stride}th row of each of the {len(frames)} frames of {args.config} ({ev_tot // args.steps} evals/step)"
+    sample = f"{sample} ({ev_tot // args.steps} active evals per step; the same sample as our arm's cpu_baseline)"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_tot / args.steps, "higher_is_better": True,
-        "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
         "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -226,13 +240,11 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
-def read_profile_traffic(config="C2"):
-    """The committed ncu evidence for this config: whole-step counts over every
-    frame of a step (profiles/ncu_counts_<config>.json, tools/ncu_step_counts.py:
-    SASS thread-instructions and DRAM bytes per pixel, averaged over the step's
-    frames, whose cost varies) and, for C2, the full capture of one frame
-    (profiles/ncu_summary.json: FP32 op counts). Returns (DRAM bytes per pixel,
-    counts dict with 'full' = the full-capture dict or None)."""
+def read_profile_traffic(config):
+    """The committed ncu evidence for this config (profiles/ncu_counts_<config>.json,
+    tools/ncu_step_counts.py: SASS thread-instructions and DRAM bytes per pixel
+    over every launch of a step) and, for C2 / C5, the full capture of one frame
+    (profiles/ncu_summary_<config>.json). Returns (DRAM bytes per pixel, counts)."""
     def load(name):
         p = os.path.join(ROOT, "profiles", name)
         if not os.path.exists(p):
@@ -240,10 +252,9 @@ def read_profile_traffic(config="C2"):
         with open(p) as f:
             return json.load(f)
     counts = load(f"ncu_counts_{config.lower()}.json")
-    full = load("ncu_summary.json") if config == "C2" else None
     if counts is None:
         return None, None
-    counts["full"] = full
+    counts["full"] = load(f"ncu_summary_{config.lower()}.json")
     return counts.get("dram_bytes_per_launch_per_pixel"), counts
 
 
@@ -274,52 +285,92 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     ctx = pkg.Context(local)
-    frames, desc = make_frames(args.config, dev, seed=1 + 1000 * rank, rank=rank, world=world)
-    for fr in frames:
-        fr.scene.draws = args.draws
-        fr.scene.method = args.method
+    n_frames, H, W, desc = WORKLOADS[args.config]
+    gen = _gen(args.config)
+    tiles = D.plan_tiles(n_frames, H, world)
+    mine = [i for i in range(len(tiles)) if i % world == rank]
+    frames = {}
+    for i in mine:
+        f, y0, y1 = tiles[i]
+        fr = gen(f, (y0, y1, 0, W), dev)
+        fr.scene.draws, fr.scene.method = args.draws, args.method
+        frames[i] = fr
     if args.draws != 48:
         desc += f"; ABLATION: {args.draws} draws per pixel-light (P:L749/L758)"
     if args.method == "zk":
         desc += "; BASELINE: Zirr & Kaplanyan-style path (DESIGN.md section 10), not the paper's method"
-    tot_px, valid_px, evals = count_evals(frames)
-    gbuf_all = None
-    if args.config == "C5" and args.gather == "p2p":
-        # every rank's kernel stores its frames straight into rank 0's buffer
-        # (CUDA IPC peer memory over NVLink): the gather is fused into shading
-        fr0 = frames[0]
-        gbuf_all = D.peer_buffer((C5_FRAMES, fr0.gbuf.height, fr0.gbuf.width, 4), device=dev)
-        outs = [gbuf_all[fr.frame_id] for fr in frames]
-    else:
-        outs = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32, device=dev) for fr in frames]
-    stream = torch.cuda.current_stream(dev)
+    L = len(next(iter(frames.values())).scene.lights) if frames else 0
 
-    gbs, scenes = [fr.gbuf for fr in frames], [fr.scene for fr in frames]
+    # ---- the metric's unit, counted outside the timed region
+    active = {i: pkg.glint_count_active(ctx, fr.gbuf, fr.scene) for i, fr in frames.items()}
+    valid = {i: fr.gbuf.valid_count() for i, fr in frames.items()}
+    evals = sum(active.values())
+    evals_replicated = sum(valid[i] * len(frames[i].scene.lights) for i in frames)
+    px = sum(frames[i].gbuf.height * frames[i].gbuf.width for i in frames)
+
+    # ---- outputs: rank 0 owns the step's full frames; the gather is in the timed region
+    use_nccl = world > 1 and args.gather == "nccl"
+    comm = torch.cuda.Stream(dev) if use_nccl else None
+    if use_nccl:
+        full = torch.empty((n_frames, H, W, 4), dtype=torch.float32, device=dev) if rank == 0 else None
+        gatherer = D.TileGather(tiles, rank, world, full=full, comm_stream=comm)
+        local_outs = {} if rank == 0 else {i: torch.empty((tiles[i][2] - tiles[i][1], W, 4), dtype=torch.float32,
+                                                          device=dev) for i in mine}
+        outs = [full[tiles[i][0]] if rank == 0 else local_outs[i] for i in mine]
+        origins = [(0, tiles[i][1]) if rank == 0 else (0, 0) for i in mine]
+    else:
+        full = D.peer_buffer((n_frames, H, W, 4), device=dev)     # rank 0's buffer, mapped everywhere
+        outs = [full[tiles[i][0]] for i in mine]
+        origins = [(0, tiles[i][1]) for i in mine]
+    gbs = [frames[i].gbuf for i in mine]
+    scenes = [frames[i].scene for i in mine]
+    stream = torch.cuda.current_stream(dev)
+    comm_done = torch.cuda.Event() if use_nccl else None
 
     def step(evs=None):
-        if evs is None and not args.no_batch:
-            # the step's frames in one call: launches chained with programmatic
-            # dependent launch (frame f+1 fills the SMs frame f frees at its tail)
-            pkg.glint_eval_batch(ctx, gbs, scenes, outs=outs, stream=stream)
+        if use_nccl:
+            tile_ev = {}
+            for k, i in enumerate(mine):
+                pkg.glint_eval_batch(ctx, [gbs[k]], [scenes[k]], outs=[outs[k]], stream=stream, origins=[origins[k]])
+                e = torch.cuda.Event()
+                e.record(stream)
+                tile_ev[i] = e
+            works = gatherer.run({i: outs[k] for k, i in enumerate(mine)} if rank != 0 else {}, tile_ev)
+            with torch.cuda.stream(comm):
+                for w in works:
+                    w.wait()
+                comm_done.record(comm)
+            # the step ends when its gather has landed (and the next step's kernels
+            # may then overwrite the local buffers the sends read)
+            stream.wait_event(comm_done)
             return
-        for i, (fr, out) in enumerate(zip(frames, outs)):
+        if evs is None and not args.no_batch:
+            # this rank's tiles in one call: launches chained with programmatic
+            # dependent launch (tile t+1 fills the SMs tile t frees at its tail)
+            pkg.glint_eval_batch(ctx, gbs, scenes, outs=outs, stream=stream, origins=origins)
+            return
+        for k in range(len(mine)):
             if evs is not None:
-                evs[i][0].record(stream)
-            pkg.glint_eval(ctx, fr.gbuf, fr.scene, out=out, stream=stream)
+                evs[k][0].record(stream)
+            pkg.glint_eval(ctx, gbs[k], scenes[k], out=outs[k], stream=stream, origin=origins[k])
             if evs is not None:
-                evs[i][1].record(stream)
+                evs[k][1].record(stream)
 
     args.warmup = max(args.warmup, 3)      # contract: W >= 3
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    D.barrier()
 
-    # per-launch durations of the serialised launches (CUDA events between
-    # launches; outside the timed region, which chains them): median / min
-    ev_pairs = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in frames]
-    step(ev_pairs)
-    torch.cuda.synchronize()
-    serial_launch_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+    # per-launch durations of serialised launches (outside the timed region)
+    ev_pairs = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in mine]
+    if not use_nccl:
+        step(ev_pairs)
+        torch.cuda.synchronize()
+        serial_launch_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+    else:
+        serial_launch_ms = [float("nan")]
+    D.barrier()
 
     def timed():
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -329,22 +380,47 @@ def run_ours(args):
             torch.cuda.synchronize()
             torch.cuda.nvtx.range_push("glint_timed")   # ncu --nvtx-include "glint_timed/": the step's launches
             start.record(stream)
-            for k in range(args.steps):
+            for _ in range(args.steps):
                 step()
             end.record(stream)
             torch.cuda.nvtx.range_pop()
             torch.cuda.synchronize()
             D.barrier()
-        ms = start.elapsed_time(end)
-        return ms, ctx.launch_count() - n0, clk
+        return start.elapsed_time(end), ctx.launch_count() - n0, clk
 
     ms, launches, clk = timed()
     if clk.rejected():
         ms, launches, clk = timed()
     ms_max = D.max_over_ranks(ms, device=dev)
-    evals_all = D.sum_over_ranks(evals * args.steps, device=dev)
-    launches_all = int(round(D.sum_over_ranks(float(launches), device=dev)))   # every rank's kernels
+    evals_all = D.sum_over_ranks(evals, device=dev) * args.steps
+    evals_repl_all = D.sum_over_ranks(evals_replicated, device=dev) * args.steps
+    launches_all = int(round(D.sum_over_ranks(float(launches), device=dev)))
     value = evals_all / (ms_max / 1e3)
+
+    # ---- verification of the gathered step: rank 0's frames all written, and
+    # tiles shaded on other ranks equal rank 0's own evaluation bit for bit
+    if rank == 0:
+        full.fill_(float("nan"))
+        torch.cuda.synchronize()
+    D.barrier()
+    step()
+    torch.cuda.synchronize()
+    D.barrier()
+    check = None
+    if rank == 0:
+        assert not torch.isnan(full[..., 3]).any().item(), "a pixel of the gathered frames was never written"
+        remote = [i for i in range(len(tiles)) if i % world != 0][:3]
+        for i in remote:
+            f, y0, y1 = tiles[i]
+            fr = gen(f, (y0, y1, 0, W), dev)
+            fr.scene.draws, fr.scene.method = args.draws, args.method
+            ref = pkg.glint_eval(ctx, fr.gbuf, fr.scene)
+            torch.cuda.synchronize()
+            if not torch.equal(ref.view(torch.int32), full[f][y0:y1].view(torch.int32)):
+                raise SystemExit(f"tile {i} gathered from rank {i % world} differs from rank 0's evaluation")
+        check = (f"all {n_frames} frames written at rank 0; {len(remote)} tiles from other ranks "
+                 f"re-evaluated on rank 0: bit-identical") if remote else f"all {n_frames} frames written"
+    D.barrier()
 
     # ---- roofline of the dominant (only) kernel: issue-bound ALU path
     peaks, peak_src = load_peaks()
@@ -352,48 +428,42 @@ def run_ours(args):
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
     issue_peak = sms * LANES_PER_SM * f_max                   # thread-instructions/s
-    L = len(frames[0].scene.lights)
-    w_eval = W_EVAL + W_PIXEL / L
+    w_eval = W_EVAL + W_PIXEL / max(L, 1)
+    launches_per_step = len(mine)
     # the kernel's average launch duration inside the timed region: the
     # launches are back to back on one stream (chained, so one launch's tail
-    # overlaps the next one's start), so step time / launches per step
-    mean_launch_s = ms / 1e3 / launches
-    evals_per_launch = evals / len(frames)
+    # overlaps the next one's start): this rank's step time / its launches
+    mean_launch_s = ms / 1e3 / max(launches, 1)
+    evals_per_launch = evals / max(launches_per_step, 1)
     achieved = evals_per_launch * w_eval / mean_launch_s
     traffic_pp, prof = read_profile_traffic(args.config)
-    px_per_launch = tot_px / len(frames)
+    px_per_launch = px / max(launches_per_step, 1)
     roofline = {
         "bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "thread-inst/s",
         "frac": achieved / issue_peak,
         "traffic": (traffic_pp * px_per_launch) if traffic_pp else None,
         "peak_source": f"{sms} SMs x 128 lanes x sm_max_mhz {f_max / 1e6:.0f} ({peak_src} MEASURED_PEAKS.json)",
         "algorithmic_inst_per_eval": w_eval,
+        "evals_per_launch": evals_per_launch,
         "hbm_achieved_gbs": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9,
         "hbm_frac": BYTES_PER_PIXEL * px_per_launch / mean_launch_s / 1e9 / float(peaks.get("hbm_gbs", 6458.7)),
         "mean_launch_ms": mean_launch_s * 1e3,
-        "launch_ms_basis": "timed region / launches (chained launches of glint_eval_batch)" if not args.no_batch
-        else "timed region / launches (one glint_eval per frame)",
-        "serial_median_launch_ms": float(np.median(serial_launch_ms)),
-        "serial_min_launch_ms": float(np.min(serial_launch_ms)),
+        "launch_ms_basis": "rank 0's timed region / its launches (glint_eval_batch: chained launches)",
+        "serial_median_launch_ms": float(np.nanmedian(serial_launch_ms)) if not use_nccl else None,
+        "serial_min_launch_ms": float(np.nanmin(serial_launch_ms)) if not use_nccl else None,
     }
-    # the committed ncu evidence is per config, for the method (48 draws):
-    # its per-pixel SASS count applies to that workload only
     if prof and prof.get("sass_thread_inst_per_pixel") and args.draws == 48 and args.method == "ours":
-        # issue utilisation from the measured SASS count averaged over the step
         roofline["sass_thread_inst_per_pixel"] = prof["sass_thread_inst_per_pixel"]
         roofline["issue_frac_sass"] = px_per_launch * prof["sass_thread_inst_per_pixel"] / mean_launch_s / issue_peak
         if prof.get("warp_inst_per_pixel"):
-            # issue-slot utilisation proper (smsp__inst_executed / (4 x SMs x cycles)): a
-            # warp instruction takes one slot however many lanes are active or predicated on
             roofline["warp_inst_per_pixel"] = prof["warp_inst_per_pixel"]
             roofline["issue_frac_warp"] = px_per_launch * prof["warp_inst_per_pixel"] / mean_launch_s / (sms * 4 * f_max)
         roofline["traffic_source"] = (f"profiles/ncu_counts_{args.config.lower()}.json ({prof.get('source')}, "
                                       f"{prof.get('launches')} launches: every frame of a step)")
-        full = prof.get("full")
-        if full and full.get("fp32_flop_per_pixel") and full.get("sass_thread_inst_per_pixel"):
-            # FP32 arithmetic vs 2 x 128 x SMs x f (not the bound: ALU/issue is);
-            # the full capture's FP32 share of its frame's instructions, applied to the step's count
-            fl_pp = full["fp32_flop_per_pixel"] * prof["sass_thread_inst_per_pixel"] / full["sass_thread_inst_per_pixel"]
+        full_cap = prof.get("full")
+        if full_cap and full_cap.get("fp32_flop_per_pixel") and full_cap.get("sass_thread_inst_per_pixel"):
+            fl_pp = (full_cap["fp32_flop_per_pixel"] * prof["sass_thread_inst_per_pixel"]
+                     / full_cap["sass_thread_inst_per_pixel"])
             fl = px_per_launch * fl_pp / mean_launch_s
             roofline["fp32_tflops"] = fl / 1e12
             roofline["fp32_frac"] = fl / (2 * sms * LANES_PER_SM * f_max)
@@ -401,47 +471,23 @@ def run_ours(args):
     if cs.get("sm_mhz"):
         roofline["frac_at_measured_clock"] = achieved / (sms * LANES_PER_SM * cs["sm_mhz"] * 1e6)
 
-    # ---- end to end through the public C ABI with host buffers
-    # ---- C5: gather every frame's radiance to rank 0 (NCCL p2p), timed apart
-    gather = None
-    if args.config == "C5" and args.gather == "p2p":
-        D.barrier()
-        torch.cuda.synchronize()
-        if rank == 0:   # every frame landed: flags plane of each frame written
-            assert not torch.isnan(gbuf_all[..., 3]).any().item()
-        gather = {"ms": 0.0, "frames": C5_FRAMES, "bytes": int(gbuf_all.numel() * 4) if rank == 0 else None,
-                  "how": "fused: each rank's kernel stores its frames' radiance directly into rank 0's buffer "
-                         "(CUDA IPC peer memory over NVLink), inside the timed region"}
-    elif args.config == "C5":
-        D.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        full = D.gather_frames({fr.frame_id: o for fr, o in zip(frames, outs)}, range(C5_FRAMES),
-                               shape=tuple(outs[0].shape), device=dev)
-        torch.cuda.synchronize()
-        t_g = D.max_over_ranks(time.perf_counter() - t0, device=dev)
-        if rank == 0 and sorted(full) != list(range(C5_FRAMES)):
-            raise SystemExit("C5 gather incomplete")
-        gather = {"ms": t_g * 1e3, "frames": C5_FRAMES, "bytes": int(C5_FRAMES * outs[0].numel() * 4),
-                  "how": "torch.distributed send/recv per frame to rank 0, after the timed region"}
-        del full
-
+    # ---- end to end through the public C ABI with host buffers (each rank
+    # its own tiles: pinned host G-buffers in, host radiance out)
     e2e = None
     if not args.no_e2e:
-        # C5: the first 4 of this rank's frames (pinning 42 GB of host G-buffer is not sensible)
-        sub_n = 4 if args.config == "C5" else len(frames)
-        hosts = [fr.gbuf.to("cpu").pin() for fr in frames[:sub_n]]
-        houts = [torch.empty((fr.gbuf.height, fr.gbuf.width, 4), dtype=torch.float32).pin_memory()
-                 for fr in frames[:sub_n]]
-        e_px, _, e_ev = count_evals(frames[:sub_n])
+        sub = mine[:args.e2e_tiles if args.e2e_tiles else (4 if H >= 2160 else 10)]
+        hosts = [frames[i].gbuf.to("cpu").pin() for i in sub]
+        houts = [torch.empty((frames[i].gbuf.height, W, 4), dtype=torch.float32).pin_memory() for i in sub]
+        e_px = sum(frames[i].gbuf.height * W for i in sub)
+        e_ev = sum(active[i] for i in sub)
         n_e2e = max(1, min(args.steps, args.e2e_steps))
-        e_scenes = [fr.scene for fr in frames[:sub_n]]
+        e_scenes = [frames[i].scene for i in sub]
 
         def e2e_step():
             if args.no_batch:
                 for hb, sc, ho in zip(hosts, e_scenes, houts):
                     pkg.glint_eval_host(ctx, hb, sc, out=ho)
-            else:   # one call per step: the copy/compute pipeline runs across the frames
+            else:   # one call per step: the copy/compute pipeline runs across the tiles
                 pkg.glint_eval_host_batch(ctx, hosts, e_scenes, outs=houts)
         e2e_step()
         D.barrier()
@@ -452,54 +498,58 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_e2e = D.max_over_ranks(time.perf_counter() - t0, device=dev)
         e2e = {"value": D.sum_over_ranks(e_ev * n_e2e, device=dev) / t_e2e, "unit": UNIT,
-               "h2d_bytes_per_step": int(e_px * 80), "d2h_bytes_per_step": int(e_px * 16),
+               "h2d_bytes_per_step": int(D.sum_over_ranks(e_px * 80, device=dev)),
+               "d2h_bytes_per_step": int(D.sum_over_ranks(e_px * 16, device=dev)),
                "steps": n_e2e, "api": ("glint_eval_host" if args.no_batch else "glint_eval_host_batch")
-               + " (pinned host G-buffers -> host radiance)"}
-        if sub_n < len(frames):
-            e2e["sample"] = f"first {sub_n} of this rank's {len(frames)} frames"
-        # the host link is the e2e bound: compare with a measured pinned H2D copy
+               + " (pinned host G-buffers -> host radiance), every rank on its own tiles",
+               "sample": f"first {len(sub)} of each rank's {len(mine)} tiles (host pinned memory bound)"}
         h2d_peak = measure_h2d_gbs(dev)
         e2e["h2d_gbs_achieved"] = e_px * 80 * n_e2e / t_e2e / 1e9
         e2e["h2d_gbs_measured_peak"] = h2d_peak
         e2e["h2d_frac"] = e2e["h2d_gbs_achieved"] / h2d_peak
         # sanity: host path reproduces the device path bit for bit
-        if not torch.equal(houts[0].view(torch.int32), outs[0].cpu().view(torch.int32)):
+        ref0 = pkg.glint_eval(ctx, gbs[0], scenes[0])
+        torch.cuda.synchronize()
+        if not torch.equal(houts[0].view(torch.int32), ref0.cpu().view(torch.int32)):
             raise SystemExit("host-buffer entry output differs from glint_eval")
+        del hosts, houts
 
-    # ---- CPU baseline (oracle on host cores), rank 0 at N = 1 only
+    # ---- CPU baseline (oracle on host cores, the same sample as --impl reference), rank 0 at N = 1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # bounded sample: every 2nd row of the C2 step (~10^7 evals, ~20-30 s of
-        # CPU work on 16 cores; ~2 s wall) / every 32nd row of C4
-        stride = 2 if args.config == "C2" else (32 if args.config == "C4" else 256)
-        subs = oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride)
+        subs, sample = oracle_sample(args.config)
+        for gb, sc in subs:
+            sc.draws, sc.method = args.draws, args.method
         ev, t = time_oracle(subs)
         cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-               "sample": f"every {stride}th row of each of the {len(frames)} frames ({ev} evals, {t:.1f} s wall, "
-                         f"{t * host_cores():.0f} core-s)"}
-        # the single-core figure beside the all-core one (a 16x sparser row sample)
-        ev1, t1 = time_oracle(oracle_sample([type(fr)(fr.name, fr.gbuf, fr.scene) for fr in frames], stride * 16),
-                              threads=1)
-        cpu["value_1core"] = ev1 / t1
-        cpu["sample_1core"] = f"every {stride * 16}th row, 1 thread ({ev1} evals, {t1:.1f} s)"
+               "sample": f"{sample} ({ev} active evals, {t:.1f} s wall, {t * host_cores():.0f} core-s)"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": desc, "pixels_per_step": tot_px, "valid_pixels_per_step": valid_px,
-                       "evals_per_step_per_rank": evals, "lights": L, "launches_per_step": len(frames),
-                       "launch_path": ("glint_eval (one launch per frame)" if args.no_batch else
-                                       "glint_eval_batch (one call per step; frames chained by programmatic "
-                                       "dependent launch)"),
-                       "l2": f"inputs {tot_px * 80 / 1e9:.2f} GB per rank > 126 MB L2: no flush between steps",
-                       "parallelism": ((f"64 frames sharded over {world} ranks (f = rank mod {world}); radiance "
-                                        + ("stored by the kernels straight into rank 0's buffer (peer memory)"
-                                           if args.gather == "p2p" else "gathered to rank 0 after the timed region"))
-                                       if args.config == "C5" else f"frames x{world} ranks, no data-path collective"),
-                       **({"gather": gather} if gather else {})},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "pixels_per_step_per_rank": px,
+                       "evals_per_step_per_rank": evals,
+                       "evals_replicated_per_step_per_rank": evals_replicated,
+                       "evals_note": "evals = active (pixel, light) pairs (glint_count_active: valid pixel, "
+                                     "non-degenerate footprint, light above the horizon, R-27b); replicated = "
+                                     "valid pixels x lights",
+                       "value_replicated_pairs": evals_repl_all / (ms_max / 1e3),
+                       "lights": L, "tiles_per_step": len(tiles), "launches_per_step_per_rank": launches_per_step,
+                       "launch_path": ("glint_eval (one launch per tile)" if args.no_batch else
+                                       "glint_eval_batch (one call per step and rank; tiles chained by "
+                                       "programmatic dependent launch)") if not use_nccl else
+                                      "glint_eval_batch per tile + an event, NCCL round per tile",
+                       "l2": "inputs > 126 MB L2 per rank: no flush between steps",
+                       "parallelism": (f"{len(tiles)} tiles ({'whole frames' if tiles[0][2] - tiles[0][1] == H else '64-row bands'}) "
+                                       f"dealt round-robin to {world} ranks"),
+                       "gather": ("none (one rank: the frames are shaded in place)" if world == 1 else
+                                  "fused: the kernels store every tile into rank 0's full frames (CUDA IPC peer "
+                                  "memory over NVLink), inside the timed region" if not use_nccl else
+                                  "NCCL grouped send/recv per tile round on a comm stream, each send after its "
+                                  "tile's kernel event, inside the timed region"),
+                       "verified": check},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all,
             "clocks": cs, "gpu": props.name,
         }
@@ -510,25 +560,45 @@ def run_ours(args):
     return 0
 
 
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=["C2", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=sorted(WORKLOADS))
     ap.add_argument("--method", default="ours", choices=["ours", "zk"],
                     help="ours = the paper's method; zk = the Zirr & Kaplanyan-style baseline (eval_mode 3)")
     ap.add_argument("--gather", default="p2p", choices=["p2p", "nccl"],
-                    help="C5: fuse the gather to rank 0 into the kernels (peer stores) or send/recv afterwards")
+                    help="N > 1: fuse the gather to rank 0 into the kernels (peer stores) or NCCL per tile")
     ap.add_argument("--draws", type=int, default=48, choices=[48, 64, 160],
                     help="draws per pixel-light: 48 = the method; 64 / 160 = its section-6 ablations")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-tiles", type=int, default=0,
+                    help="tiles per rank in the host-buffer (e2e) leg (default: 4 of a 4K config, else 10)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-batch", action="store_true",
-                    help="one glint_eval per frame instead of one glint_eval_batch per step (A/B)")
+                    help="one glint_eval per tile instead of one glint_eval_batch per step (A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch through torchrun
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+               *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}: refusing to report\n")
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -39,15 +39,18 @@
 extern "C" {
 #endif
 
-#define GLINT_VERSION 10000 /* 1.0.0 */
+#define GLINT_VERSION 20000 /* 2.0.0: tile origin in glint_gbuffer, glint_count_active */
 
 /* return codes */
 #define GLINT_OK 0
-#define GLINT_EINVAL -1   /* null pointer, size < 0, bad enum, K not in [1,8], beta <= 0, n_lights not in [0,16],
-                             eval_mode not in [0,3] or debug records requested with eval_mode != 0 */
+#define GLINT_EINVAL -1   /* null pointer, size < 0, tile origin < 0, bad enum, K not in [1,8], beta not finite or
+                             < 2^-20, n_lights not in [0,16], eval_mode not in [0,3] or debug records requested
+                             with eval_mode != 0 */
 #define GLINT_EALIGN -2   /* a plane / output pointer not 16-byte aligned, pitch < width */
 #define GLINT_EDEVICE -3  /* no CUDA device, device is not sm_100, or ctx/device mismatch */
-#define GLINT_ELIMIT -4   /* width*height or pitch*height >= 2^31 pixels */
+#define GLINT_ELIMIT -4   /* width*height >= 2^31 pixels, pitch*height (or the output's (y0+height)*out_pitch)
+                             >= 2^40 float4, or the context's pool of 4096 graph-captured launch slots is
+                             used up */
 #define GLINT_ECUDA -5    /* a CUDA runtime call failed; see glint_last_cuda_error() */
 #define GLINT_ENOMEM -6   /* host or device allocation failed */
 #define GLINT_EALIAS -7   /* glint_eval_batch / glint_eval_host_batch: an output overlaps an input plane or
@@ -67,7 +70,10 @@ extern "C" {
 typedef struct glint_ctx glint_ctx;
 
 /* A punctual light. kind 0 = point at pos_or_dir (E = I / d^2),
- * kind 1 = directional, pos_or_dir points toward the light (E = I). */
+ * kind 1 = directional, pos_or_dir points toward the light (E = I).
+ * Intensity domain: any finite value; the radiance is formed in fp64 and
+ * rounded to fp32 once per light (so it reads +inf, never NaN, where the true
+ * value exceeds fp32's range). */
 typedef struct {
   int32_t kind;
   float pos_or_dir[3];
@@ -121,6 +127,10 @@ typedef struct {
   int32_t width;
   int32_t height;
   int64_t pitch;
+  int32_t x0, y0;   /* tile origin in the output image (>= 0): pixel (x, y) of these planes is written to
+                       out[(y0 + y) * out_pitch + x0 + x]. {0, 0} for a whole frame; a row band or tile
+                       of a sharded frame passes its position so that its radiance lands in
+                       place in a full-frame output (local, or a peer GPU's mapped buffer) */
 } glint_gbuffer;
 
 /* Optional per (pixel, light) debug record (168 words, 672 bytes), written
@@ -164,16 +174,20 @@ int glint_create(glint_ctx** out, int device);
 int glint_destroy(glint_ctx* ctx);   /* waits for the device (cudaDeviceSynchronize), then frees */
 
 /* Evaluate every pixel of `gb` (device planes) for every light of `scene`:
- * out[y * out_pitch + x] = float4(R, G, B, flags bits) for all pixels (fully
- * overwritten). `out` may be any address the current device can store to:
+ * out[(gb->y0 + y) * out_pitch + gb->x0 + x] = float4(R, G, B, flags bits) for
+ * all pixels of the tile (fully overwritten; nothing else is written). `out` may be any address the current device can store to:
  * its own memory, or a peer GPU's buffer mapped through CUDA IPC / peer
  * access (the kernel then streams the radiance over NVLink -- the fused
  * gather of DESIGN.md section 8). `dbg` (device, nullable) receives
  * width*height*n_lights records. One kernel launch on `stream`; asynchronous;
  * no host synchronisation or allocation, so it can be captured in a CUDA
- * graph. Each launch owns one slot of a ring of 1024 tile-scheduler counters
- * (reset by the launch itself): a captured launch keeps its slot, so one graph
- * must not be replayed concurrently with itself. */
+ * graph. Each launch owns a tile-scheduler counter pair, reset by the launch
+ * itself: an ordinary launch takes the next slot of a ring of 1024, so at most
+ * 1024 launches of one context may be in flight at once (across all streams);
+ * a launch recorded by stream capture (cudaStreamIsCapturing) gets a pair of
+ * its own from a separate pool of 4096 that is never recycled, so a graph can
+ * be replayed alongside any number of ordinary launches, but one graph must
+ * not be replayed concurrently with itself. */
 int glint_eval(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
                void* out, int64_t out_pitch, glint_debug_rec* dbg, void* stream);
 
@@ -220,6 +234,15 @@ int glint_eval_host(glint_ctx* ctx, const glint_gbuffer* gb_host, const glint_sc
  * per context like glint_eval_host. n_frames = 0 is a no-op. */
 int glint_eval_host_batch(glint_ctx* ctx, int n_frames, const glint_gbuffer* gbs_host, const glint_scene* scenes,
                           void* const* outs_host, const int64_t* out_pitches, void* stream);
+
+/* Count the (pixel, light) evaluations of `gb` under `scene`: pixels that are
+ * valid with a non-degenerate footprint (flags 0 apart from RATIO/P clamps)
+ * times the lights active there (n.wi > 0, n.wo > 0, |d|^2 in [2^-126, 2^120]:
+ * the pairs whose S5-S9 work glint_eval does, R-27b) -- the unit of
+ * the throughput metric. Adds the count to *d_count (a device uint64 the
+ * caller zeroes); one kernel launch on `stream`, asynchronous. */
+int glint_count_active(const glint_ctx* ctx, const glint_gbuffer* gb, const glint_scene* scene,
+                       unsigned long long* d_count, void* stream);
 
 /* Copies of the device-resident tables (host pointers), for parity tests. */
 int glint_get_tables(const glint_ctx* ctx, float* z, float* cosv, float* sinv);

@@ -7,7 +7,7 @@ laws on anisotropic grids, as a fused sm_100a kernel behind a C ABI.
     rgb = glint_eval(ctx, frame.gbuf, frame.scene)     # (H, W, 4) float32
 """
 from ._lib import (Context, GlintError, DEBUG_REC_DTYPE, build_tables, glint_eval, glint_eval_batch,  # noqa: F401
-                   glint_eval_host, glint_eval_host_batch,
+                   glint_eval_host, glint_eval_host_batch, glint_count_active,
                    lib, strerror, version, FLAG_INVALID, FLAG_DEGENERATE, FLAG_RATIO_CLAMPED,
                    FLAG_P_CLAMPED, FLAG_UV_RANGE)
 from . import synth  # noqa: F401

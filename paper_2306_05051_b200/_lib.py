@@ -24,7 +24,7 @@ NANG = 256
 
 EXPORTS = ["glint_version", "glint_strerror", "glint_last_cuda_error", "glint_build_tables", "glint_create",
            "glint_destroy", "glint_eval", "glint_eval_batch", "glint_eval_host", "glint_eval_host_batch",
-           "glint_get_tables", "glint_launch_count"]
+           "glint_get_tables", "glint_launch_count", "glint_count_active"]
 
 
 class GlintError(RuntimeError):
@@ -50,7 +50,8 @@ class glint_scene(C.Structure):
 
 class glint_gbuffer(C.Structure):
     _fields_ = [("duv", C.c_void_p), ("uvm", C.c_void_p), ("nrm", C.c_void_p), ("pos", C.c_void_p),
-                ("mat", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32), ("pitch", C.c_int64)]
+                ("mat", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32), ("pitch", C.c_int64),
+                ("x0", C.c_int32), ("y0", C.c_int32)]
 
 
 # glint_debug_rec (168 words) as a numpy structured dtype
@@ -104,6 +105,9 @@ def lib():
         L.glint_get_tables.restype = C.c_int
         L.glint_launch_count.argtypes = [C.c_void_p]
         L.glint_launch_count.restype = C.c_int64
+        L.glint_count_active.argtypes = [C.c_void_p, C.POINTER(glint_gbuffer), C.POINTER(glint_scene), C.c_void_p,
+                                         C.c_void_p]
+        L.glint_count_active.restype = C.c_int
         _lib = L
     return _lib
 
@@ -147,7 +151,7 @@ def scene_struct(scene) -> glint_scene:
     return s
 
 
-def _gbuffer_struct(gb) -> glint_gbuffer:
+def _gbuffer_struct(gb, origin=(0, 0)) -> glint_gbuffer:
     planes = gb.planes()
     H, W = int(planes[0].shape[0]), int(planes[0].shape[1])
     for p in planes:
@@ -161,7 +165,25 @@ def _gbuffer_struct(gb) -> glint_gbuffer:
     g = glint_gbuffer()
     g.duv, g.uvm, g.nrm, g.pos, g.mat = [p.data_ptr() for p in planes]
     g.width, g.height, g.pitch = W, H, pitch
+    g.x0, g.y0 = int(origin[0]), int(origin[1])
     return g
+
+
+def _check_out(out, g, device_type: str, what: str):
+    """The output must hold the tile at its origin: float32, (rows, cols, 4)
+    with rows >= y0 + H and cols >= x0 + W, float4 rows (stride(2) == 1,
+    stride(1) == 4, stride(0) a multiple of 4), on the right device -- else
+    the kernel or the D2H copy would write past it."""
+    import torch
+    if not isinstance(out, torch.Tensor) or out.dtype != torch.float32 or out.dim() != 3 or out.shape[2] != 4:
+        raise ValueError(f"{what}: out must be a float32 tensor of shape (rows, cols, 4)")
+    if out.device.type != device_type:
+        raise ValueError(f"{what}: out must be a {device_type} tensor")
+    if out.stride(2) != 1 or out.stride(1) != 4 or out.stride(0) % 4 != 0 or out.stride(0) < 4 * out.shape[1]:
+        raise ValueError(f"{what}: out must be a row-pitched float4 array (stride(2) == 1, stride(1) == 4)")
+    if out.shape[0] < g.y0 + g.height or out.shape[1] < g.x0 + g.width:
+        raise ValueError(f"{what}: out of shape {tuple(out.shape)} cannot hold a {g.height}x{g.width} tile at "
+                         f"origin (x0, y0) = ({g.x0}, {g.y0})")
 
 
 class Context:
@@ -209,22 +231,22 @@ class Context:
         return int(lib().glint_launch_count(self._h))
 
 
-def glint_eval(ctx: Context, gb, scene, out=None, debug: bool = False, stream=None):
+def glint_eval(ctx: Context, gb, scene, out=None, debug: bool = False, stream=None, origin=(0, 0)):
     """Shade a device-resident G-buffer (synth.GBuffer of CUDA tensors).
     Returns the (H, W, 4) float32 radiance tensor (RGB + flag bits) and, if
     ``debug``, the (H*W, n_lights) debug records as a numpy structured array
-    (copied to host, synchronising)."""
+    (copied to host, synchronising). ``origin`` = (x0, y0): the tile's place
+    in ``out`` (a larger frame; glint.h tile origin)."""
     import torch
     planes = gb.planes()
     dev = planes[0].device
     if dev.type != "cuda":
         raise ValueError("glint_eval needs CUDA tensors (use glint_eval_host for host buffers)")
-    g = _gbuffer_struct(gb)
+    g = _gbuffer_struct(gb, origin)
     sc = scene_struct(scene)
     if out is None:
-        out = torch.empty((g.height, g.width, 4), dtype=torch.float32, device=dev)
-    if out.stride(2) != 1 or out.stride(1) != 4:
-        raise ValueError("out must be a contiguous-row float4 tensor")
+        out = torch.empty((g.y0 + g.height, g.x0 + g.width, 4), dtype=torch.float32, device=dev)
+    _check_out(out, g, "cuda", "glint_eval")
     dbg = None
     if debug:
         dbg = torch.zeros(max(1, g.width * g.height * sc.n_lights * DEBUG_REC_BYTES // 4),
@@ -241,7 +263,7 @@ def glint_eval(ctx: Context, gb, scene, out=None, debug: bool = False, stream=No
     return out
 
 
-def glint_eval_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
+def glint_eval_batch(ctx: Context, gbs, scenes, outs=None, stream=None, origins=None):
     """Shade independent device-resident frames with one call (the launches
     are chained with programmatic dependent launch; include/glint.h). Frame f's
     result equals glint_eval(ctx, gbs[f], scenes[f]) bit for bit. Returns the
@@ -255,13 +277,14 @@ def glint_eval_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
     dev = gbs[0].planes()[0].device
     if any(g.planes()[0].device != dev for g in gbs) or dev.type != "cuda":
         raise ValueError("glint_eval_batch needs CUDA tensors on one device")
-    G = (glint_gbuffer * n)(*[_gbuffer_struct(g) for g in gbs])
+    origins = origins or [(0, 0)] * n
+    G = (glint_gbuffer * n)(*[_gbuffer_struct(g, o) for g, o in zip(gbs, origins)])
     S = (glint_scene * n)(*[scene_struct(sc) for sc in scenes])
     if outs is None:
-        outs = [torch.empty((G[f].height, G[f].width, 4), dtype=torch.float32, device=dev) for f in range(n)]
-    for o in outs:
-        if o.stride(2) != 1 or o.stride(1) != 4:
-            raise ValueError("out must be a contiguous-row float4 tensor")
+        outs = [torch.empty((G[f].y0 + G[f].height, G[f].x0 + G[f].width, 4), dtype=torch.float32, device=dev)
+                for f in range(n)]
+    for f, o in enumerate(outs):
+        _check_out(o, G[f], "cuda", "glint_eval_batch")
     P = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
     Q = (C.c_int64 * n)(*[o.stride(0) // 4 for o in outs])
     s = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -271,16 +294,17 @@ def glint_eval_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
     return outs
 
 
-def glint_eval_host(ctx: Context, gb, scene, out=None, stream=None):
+def glint_eval_host(ctx: Context, gb, scene, out=None, stream=None, origin=(0, 0)):
     """End-to-end: host (ideally pinned) G-buffer in, host radiance out; the
     library pipelines H2D / kernel / D2H over row chunks. Synchronous."""
     import torch
-    g = _gbuffer_struct(gb)
+    g = _gbuffer_struct(gb, origin)
     if gb.planes()[0].device.type != "cpu":
         raise ValueError("glint_eval_host needs host tensors")
     sc = scene_struct(scene)
     if out is None:
-        out = torch.empty((g.height, g.width, 4), dtype=torch.float32).pin_memory()
+        out = torch.empty((g.y0 + g.height, g.x0 + g.width, 4), dtype=torch.float32).pin_memory()
+    _check_out(out, g, "cpu", "glint_eval_host")
     s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
     rc = lib().glint_eval_host(ctx.handle, C.byref(g), C.byref(sc), out.data_ptr(), out.stride(0) // 4,
                                C.c_void_p(s.cuda_stream))
@@ -289,7 +313,7 @@ def glint_eval_host(ctx: Context, gb, scene, out=None, stream=None):
     return out
 
 
-def glint_eval_host_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
+def glint_eval_host_batch(ctx: Context, gbs, scenes, outs=None, stream=None, origins=None):
     """End-to-end over several frames: host (ideally pinned) G-buffers in,
     host radiance out, one continuous copy/compute pipeline across the frames.
     Frame f equals glint_eval_host(ctx, gbs[f], scenes[f]) bit for bit.
@@ -302,10 +326,14 @@ def glint_eval_host_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
         return []
     if any(g.planes()[0].device.type != "cpu" for g in gbs):
         raise ValueError("glint_eval_host_batch needs host tensors")
-    G = (glint_gbuffer * n)(*[_gbuffer_struct(g) for g in gbs])
+    origins = origins or [(0, 0)] * n
+    G = (glint_gbuffer * n)(*[_gbuffer_struct(g, o) for g, o in zip(gbs, origins)])
     S = (glint_scene * n)(*[scene_struct(sc) for sc in scenes])
     if outs is None:
-        outs = [torch.empty((G[f].height, G[f].width, 4), dtype=torch.float32).pin_memory() for f in range(n)]
+        outs = [torch.empty((G[f].y0 + G[f].height, G[f].x0 + G[f].width, 4), dtype=torch.float32).pin_memory()
+                for f in range(n)]
+    for f, o in enumerate(outs):
+        _check_out(o, G[f], "cpu", "glint_eval_host_batch")
     P = (C.c_void_p * n)(*[o.data_ptr() for o in outs])
     Q = (C.c_int64 * n)(*[o.stride(0) // 4 for o in outs])
     s = stream if stream is not None else torch.cuda.current_stream(ctx.device)
@@ -313,3 +341,21 @@ def glint_eval_host_batch(ctx: Context, gbs, scenes, outs=None, stream=None):
     if rc:
         raise GlintError(rc, "glint_eval_host_batch")
     return outs
+
+
+def glint_count_active(ctx: Context, gb, scene, stream=None) -> int:
+    """The number of (pixel, light) evaluations glint_eval does on ``gb``
+    (valid pixels with a non-degenerate footprint x lights active there),
+    counted on the device with the kernel's own decisions. Synchronising."""
+    import torch
+    dev = gb.planes()[0].device
+    if dev.type != "cuda":
+        raise ValueError("glint_count_active needs CUDA tensors")
+    g = _gbuffer_struct(gb)
+    sc = scene_struct(scene)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    rc = lib().glint_count_active(ctx.handle, C.byref(g), C.byref(sc), cnt.data_ptr(), C.c_void_p(s.cuda_stream))
+    if rc:
+        raise GlintError(rc, "glint_count_active")
+    return int(cnt.item())

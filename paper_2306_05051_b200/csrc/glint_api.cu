@@ -37,8 +37,9 @@ struct glint_ctx {
   float h_z[GLINT_ZQ];
   float h_cos[GLINT_NANG], h_sin[GLINT_NANG];
   std::atomic<int64_t> launches;
-  unsigned long long* d_sched;   // kSchedSlots x [tile counter, finished blocks], zeroed
-  std::atomic<int64_t> sched_next;
+  unsigned long long* d_sched;   // (kSchedSlots + kCaptureSlots) x [tile counter, finished blocks], zeroed
+  std::atomic<int64_t> sched_next;     // ring of kSchedSlots for ordinary launches
+  std::atomic<int64_t> capture_next;   // pool of kCaptureSlots for graph-captured launches (never recycled)
   // glint_eval_host staging (2 buffers x (5 planes + out)), grown on demand
   size_t stage_px;
   float4* d_stage[2][6];
@@ -56,7 +57,7 @@ extern "C" const char* glint_strerror(int code) {
     case GLINT_EINVAL: return "invalid argument";
     case GLINT_EALIGN: return "pointer not 16-byte aligned or pitch < width";
     case GLINT_EDEVICE: return "no suitable sm_100 device / context-device mismatch";
-    case GLINT_ELIMIT: return "image too large (>= 2^31 pixels)";
+    case GLINT_ELIMIT: return "image too large (>= 2^31 pixels or >= 2^40 float4 spans), or graph-capture slots exhausted";
     case GLINT_ECUDA: return "CUDA runtime error (see glint_last_cuda_error)";
     case GLINT_ENOMEM: return "allocation failed";
     default: return "unknown error";
@@ -121,6 +122,7 @@ extern "C" int glint_create(glint_ctx** out, int device) {
   c->sm_count = prop.multiProcessorCount;
   c->launches = 0;
   c->sched_next = 0;
+  c->capture_next = 0;
   int rc = GLINT_OK;
   float2 cs[GLINT_NANG];
   glint_build_tables(c->h_z, c->h_cos, c->h_sin);
@@ -128,8 +130,9 @@ extern "C" int glint_create(glint_ctx** out, int device) {
   cudaError_t e = glint::occupancy_blocks_per_sm(&c->blocks_per_sm);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_z, sizeof(float) * GLINT_ZQ);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_cs, sizeof(float2) * GLINT_NANG);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_sched, sizeof(unsigned long long) * 2 * glint::kSchedSlots);
-  if (e == cudaSuccess) e = cudaMemset(c->d_sched, 0, sizeof(unsigned long long) * 2 * glint::kSchedSlots);
+  const size_t sched_bytes = sizeof(unsigned long long) * 2 * (glint::kSchedSlots + glint::kCaptureSlots);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_sched, sched_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->d_sched, 0, sched_bytes);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_z, c->h_z, sizeof(float) * GLINT_ZQ, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemcpy(c->d_cs, cs, sizeof(float2) * GLINT_NANG, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -217,7 +220,7 @@ static int validate_scene(const glint_scene* s) {
 
 static int validate_gbuffer(const glint_gbuffer* g, int64_t out_pitch) {
   if (!g) return GLINT_EINVAL;
-  if (g->width < 0 || g->height < 0) return GLINT_EINVAL;
+  if (g->width < 0 || g->height < 0 || g->x0 < 0 || g->y0 < 0) return GLINT_EINVAL;
   if (g->width == 0 || g->height == 0) return GLINT_OK;
   if (!g->duv || !g->uvm || !g->nrm || !g->pos || !g->mat) return GLINT_EINVAL;
   if (g->pitch < g->width || out_pitch < g->width) return GLINT_EALIGN;
@@ -225,22 +228,46 @@ static int validate_gbuffer(const glint_gbuffer* g, int64_t out_pitch) {
     return GLINT_EALIGN;
   if ((int64_t)g->width * g->height >= (int64_t)1 << 31) return GLINT_ELIMIT;
   if (g->pitch * (int64_t)g->height >= (int64_t)1 << 40) return GLINT_ELIMIT;
+  if (out_pitch >= (int64_t)1 << 40 || ((int64_t)g->y0 + g->height) * out_pitch + g->x0 >= (int64_t)1 << 40)
+    return GLINT_ELIMIT;
   return GLINT_OK;
 }
 
-static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc,
-                                  void* out, int64_t out_pitch, glint_debug_rec* dbg) {
-  // a scheduler slot per launch (ring): concurrent launches on other streams
-  // use other slots; a slot is reused kSchedSlots launches later
+// the tile's first output element: out + y0 * out_pitch + x0 (float4)
+static void* tile_out(void* out, const glint_gbuffer* g, int64_t out_pitch) {
+  return (void*)((float4*)out + (int64_t)g->y0 * out_pitch + g->x0);
+}
+
+// A scheduler counter pair for this launch: ordinary launches take the next
+// slot of a ring (reused kSchedSlots launches later); a launch recorded by
+// stream capture owns a slot of a separate pool for good (its graph may be
+// replayed at any time alongside ordinary launches).
+static int sched_slots(const glint_ctx* c, cudaStream_t stream, int n, std::vector<unsigned long long*>& slots) {
   glint_ctx* cm = const_cast<glint_ctx*>(c);
-  const int64_t slot = cm->sched_next.fetch_add(1) % glint::kSchedSlots;
-  glint::KParams k;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  GL_CUDA(cudaStreamIsCapturing(stream, &st));
+  slots.resize(n);
+  if (st == cudaStreamCaptureStatusActive) {
+    const int64_t k = cm->capture_next.fetch_add(n);
+    if (k + n > glint::kCaptureSlots) return GLINT_ELIMIT;
+    for (int i = 0; i < n; ++i) slots[i] = c->d_sched + 2 * (glint::kSchedSlots + k + i);
+  } else {
+    const int64_t k = cm->sched_next.fetch_add(n);
+    for (int i = 0; i < n; ++i) slots[i] = c->d_sched + 2 * ((k + i) % glint::kSchedSlots);
+  }
+  return GLINT_OK;
+}
+
+static void make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out,
+                        int64_t out_pitch, glint_debug_rec* dbg, unsigned long long* slot, glint::KParams* kp) {
+  glint::KParams& k = *kp;
+  k.sched = slot;
   k.duv = (const float4*)gb->duv;
   k.uvm = (const float4*)gb->uvm;
   k.nrm = (const float4*)gb->nrm;
   k.pos = (const float4*)gb->pos;
   k.mat = (const float4*)gb->mat;
-  k.out = (float4*)out;
+  k.out = (float4*)tile_out(out, gb, out_pitch);
   k.dbg = dbg;
   k.ztab = c->d_z;
   k.cstab = c->d_cs;
@@ -250,9 +277,7 @@ static glint::KParams make_params(const glint_ctx* c, const glint_gbuffer* gb, c
   k.out_pitch = out_pitch;
   k.c1s = 0x7feb352du;   // the draw hash's first multiplier, twice (see KParams)
   k.c1n = 0x7feb352du;
-  k.sched = c->d_sched + 2 * slot;
   k.sc = *sc;
-  return k;
 }
 
 static int grid_for(const glint_ctx* c, int64_t n_pix) {
@@ -278,7 +303,15 @@ extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const gli
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
-  glint::KParams k = make_params(c, gb, sc, out, out_pitch, dbg);
+  std::vector<unsigned long long*> slot;
+  try {
+    rc = sched_slots(c, (cudaStream_t)stream, 1, slot);
+  } catch (...) {
+    return GLINT_ENOMEM;
+  }
+  if (rc) return rc;
+  glint::KParams k;
+  make_params(c, gb, sc, out, out_pitch, dbg, slot[0], &k);
   int64_t n_pix = (int64_t)gb->width * gb->height;
   GL_CUDA(glint::launch_eval(k, grid_for(c, n_pix), dbg != nullptr, (cudaStream_t)stream));
   const_cast<glint_ctx*>(c)->launches++;
@@ -332,7 +365,7 @@ static int validate_batch_impl(int n_frames, const glint_gbuffer* gbs, const gli
     if (g.width == 0 || g.height == 0) continue;
     if (!outs[f]) return GLINT_EINVAL;
     if (!aligned16(outs[f])) return GLINT_EALIGN;
-    outr.push_back(plane_range(outs[f], out_pitches[f], g.width, g.height));
+    outr.push_back(plane_range(tile_out(outs[f], &g, out_pitches[f]), out_pitches[f], g.width, g.height));
     for (const void* p : {g.duv, g.uvm, g.nrm, g.pos, g.mat}) inr.push_back(plane_range(p, g.pitch, g.width, g.height));
   }
   for (size_t a = 0; a < outr.size(); ++a) {
@@ -365,14 +398,24 @@ extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gb
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
-  bool first = true;
+  int n_launch = 0;
+  for (int f = 0; f < n_frames; ++f) n_launch += (gbs[f].width > 0 && gbs[f].height > 0) ? 1 : 0;
+  std::vector<unsigned long long*> slots;
+  try {
+    rc = sched_slots(c, (cudaStream_t)stream, n_launch, slots);
+  } catch (...) {
+    return GLINT_ENOMEM;
+  }
+  if (rc) return rc;
+  int i = 0;
   for (int f = 0; f < n_frames; ++f) {
     const glint_gbuffer& g = gbs[f];
     if (g.width == 0 || g.height == 0) continue;
-    glint::KParams k = make_params(c, &g, &scenes[f], outs[f], out_pitches[f], nullptr);
-    GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)g.width * g.height), false, (cudaStream_t)stream, !first));
+    glint::KParams k;
+    make_params(c, &g, &scenes[f], outs[f], out_pitches[f], nullptr, slots[i], &k);
+    GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)g.width * g.height), false, (cudaStream_t)stream, i > 0));
     const_cast<glint_ctx*>(c)->launches++;
-    first = false;
+    ++i;
   }
   return GLINT_OK;
 }
@@ -397,6 +440,55 @@ static int ensure_stage(glint_ctx* c, size_t px) {
       if (e != cudaSuccess) { g_last_cuda = (int)e; free_stage(c); return GLINT_ENOMEM; }
     }
   c->stage_px = px;
+  return GLINT_OK;
+}
+
+// The enqueue part of host_pipeline: H2D of each row chunk into staging
+// buffer b = chunk & 1, the kernel, D2H into the caller's output (at the
+// frame's tile origin) -- all on internal stream b. Returns at the first error.
+static int host_pipeline_enqueue(glint_ctx* c, int n, const glint_gbuffer* gbs, const glint_scene* scs,
+                                 void* const* outs, const int64_t* out_pitches, void* stream, int64_t chunk_px) {
+  GL_CUDA(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
+  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamWaitEvent(c->st[b], c->ev_in, 0));
+  int chunk = 0;
+  for (int f = 0; f < n; ++f) {
+    const glint_gbuffer* gb = &gbs[f];
+    const int W = gb->width, H = gb->height;
+    if (W == 0 || H == 0) continue;
+    int rows = (int)(chunk_px / W);
+    rows = rows < 1 ? 1 : (rows > H ? H : rows);
+    const void* planes[5] = {gb->duv, gb->uvm, gb->nrm, gb->pos, gb->mat};
+    const size_t rowb = (size_t)W * sizeof(float4);
+    float4* out_tile = (float4*)tile_out(outs[f], gb, out_pitches[f]);
+    for (int y0 = 0; y0 < H; y0 += rows, ++chunk) {
+      const int b = chunk & 1;
+      const int nr = (y0 + rows <= H) ? rows : H - y0;
+      cudaStream_t s = c->st[b];
+      for (int p = 0; p < 5; ++p)
+        GL_CUDA(cudaMemcpy2DAsync(c->d_stage[b][p], rowb, (const float4*)planes[p] + (int64_t)y0 * gb->pitch,
+                                  (size_t)gb->pitch * sizeof(float4), rowb, nr, cudaMemcpyHostToDevice, s));
+      glint_gbuffer sub;
+      sub.duv = c->d_stage[b][0];
+      sub.uvm = c->d_stage[b][1];
+      sub.nrm = c->d_stage[b][2];
+      sub.pos = c->d_stage[b][3];
+      sub.mat = c->d_stage[b][4];
+      sub.width = W;
+      sub.height = nr;
+      sub.pitch = W;
+      sub.x0 = 0;
+      sub.y0 = 0;
+      std::vector<unsigned long long*> slot;
+      int rc = sched_slots(c, s, 1, slot);
+      if (rc) return rc;
+      glint::KParams k;
+      make_params(c, &sub, &scs[f], c->d_stage[b][5], W, nullptr, slot[0], &k);
+      GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
+      c->launches++;
+      GL_CUDA(cudaMemcpy2DAsync(out_tile + (int64_t)y0 * out_pitches[f], (size_t)out_pitches[f] * sizeof(float4),
+                                c->d_stage[b][5], rowb, rowb, nr, cudaMemcpyDeviceToHost, s));
+    }
+  }
   return GLINT_OK;
 }
 
@@ -431,43 +523,22 @@ static int host_pipeline(glint_ctx* c, int n, const glint_gbuffer* gbs, const gl
   if (stage_px == 0) return GLINT_OK;
   int rc = ensure_stage(c, stage_px);
   if (rc) return rc;
-  GL_CUDA(cudaEventRecord(c->ev_in, (cudaStream_t)stream));
-  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamWaitEvent(c->st[b], c->ev_in, 0));
-  int chunk = 0;
-  for (int f = 0; f < n; ++f) {
-    const glint_gbuffer* gb = &gbs[f];
-    const int W = gb->width, H = gb->height;
-    if (W == 0 || H == 0) continue;
-    int rows = (int)(chunk_px / W);
-    rows = rows < 1 ? 1 : (rows > H ? H : rows);
-    const void* planes[5] = {gb->duv, gb->uvm, gb->nrm, gb->pos, gb->mat};
-    const size_t rowb = (size_t)W * sizeof(float4);
-    for (int y0 = 0; y0 < H; y0 += rows, ++chunk) {
-      const int b = chunk & 1;
-      const int nr = (y0 + rows <= H) ? rows : H - y0;
-      cudaStream_t s = c->st[b];
-      for (int p = 0; p < 5; ++p)
-        GL_CUDA(cudaMemcpy2DAsync(c->d_stage[b][p], rowb, (const float4*)planes[p] + (int64_t)y0 * gb->pitch,
-                                  (size_t)gb->pitch * sizeof(float4), rowb, nr, cudaMemcpyHostToDevice, s));
-      glint_gbuffer sub;
-      sub.duv = c->d_stage[b][0];
-      sub.uvm = c->d_stage[b][1];
-      sub.nrm = c->d_stage[b][2];
-      sub.pos = c->d_stage[b][3];
-      sub.mat = c->d_stage[b][4];
-      sub.width = W;
-      sub.height = nr;
-      sub.pitch = W;
-      glint::KParams k = make_params(c, &sub, &scs[f], c->d_stage[b][5], W, nullptr);
-      GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
-      c->launches++;
-      GL_CUDA(cudaMemcpy2DAsync((float4*)outs[f] + (int64_t)y0 * out_pitches[f],
-                                (size_t)out_pitches[f] * sizeof(float4), c->d_stage[b][5], rowb, rowb, nr,
-                                cudaMemcpyDeviceToHost, s));
+  // from the first enqueue on, an error must not return while earlier chunks'
+  // copies into the caller's host buffers are still in flight (the call is
+  // synchronous): drain both internal streams, keep the first error
+  try {
+    rc = host_pipeline_enqueue(c, n, gbs, scs, outs, out_pitches, stream, chunk_px);
+  } catch (...) {
+    rc = GLINT_ENOMEM;
+  }
+  for (int b = 0; b < 2; ++b) {
+    const cudaError_t e = cudaStreamSynchronize(c->st[b]);
+    if (e != cudaSuccess && rc == GLINT_OK) {
+      g_last_cuda = (int)e;
+      rc = GLINT_ECUDA;
     }
   }
-  for (int b = 0; b < 2; ++b) GL_CUDA(cudaStreamSynchronize(c->st[b]));
-  return GLINT_OK;
+  return rc;
 }
 
 extern "C" int glint_eval_host(glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out_host,
@@ -499,4 +570,29 @@ extern "C" int glint_eval_host_batch(glint_ctx* c, int n_frames, const glint_gbu
   if (cur != c->device) return GLINT_EDEVICE;
   std::lock_guard<std::mutex> lock(c->host_mu);
   return host_pipeline(c, n_frames, gbs, scenes, outs, out_pitches, stream);
+}
+
+// ---------------------------------------------------------------------------
+// glint_count_active: the throughput metric's unit, counted on the device
+// with the kernel's own decision functions
+// ---------------------------------------------------------------------------
+extern "C" int glint_count_active(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc,
+                                  unsigned long long* d_count, void* stream) {
+  if (!c || !d_count) return GLINT_EINVAL;
+  int rc = validate_scene(sc);
+  if (rc) return rc;
+  rc = validate_gbuffer(gb, gb ? gb->width : 0);
+  if (rc) return rc;
+  if (gb->width == 0 || gb->height == 0) return GLINT_OK;
+  int cur = -1;
+  GL_CUDA(cudaGetDevice(&cur));
+  if (cur != c->device) return GLINT_EDEVICE;
+  const int64_t n_pix = (int64_t)gb->width * gb->height;
+  int64_t grid = (n_pix + 255) / 256;
+  const int64_t cap = (int64_t)c->sm_count * 8;
+  grid = grid < cap ? grid : cap;
+  GL_CUDA(glint::launch_count_active((const float4*)gb->duv, (const float4*)gb->uvm, (const float4*)gb->nrm,
+                                     (const float4*)gb->pos, gb->width, gb->height, gb->pitch, *sc, d_count,
+                                     (int)grid, (cudaStream_t)stream));
+  return GLINT_OK;
 }

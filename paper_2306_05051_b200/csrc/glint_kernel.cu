@@ -184,19 +184,150 @@ __device__ __forceinline__ void lattice10(float P, float r, float psi, int K, in
   }
 }
 
-// fp32 Smith Lambda for the radiance path (R-21)
-// (tolerance path: MUFU-based approximations, |rel err| ~1e-7)
-__device__ __forceinline__ float smith_lambda(int kind, float ax2, float ay2, float wx, float wy, float wz) {
-  const float s = __fmaf_rn(ax2, wx * wx, ay2 * (wy * wy));
-  if (!(s > 0.0f)) return 0.0f;
+// ---------------------------------------------------------------------------
+// Decisions shared by the shading kernel and the evaluation counter (so both
+// take them with the same operations): S1 footprint moments and validity
+// (R-7, R-25, R-30b), the S5 viewer and the per-light activity test
+// (R-27, R-27b).
+// ---------------------------------------------------------------------------
+struct Foot {
+  float P, lam, a, b, c;
+};
+__device__ __forceinline__ Foot s1_moments(float4 duv) {
+  const float dudx = duv.x, dvdx = duv.y, dudy = duv.z, dvdy = duv.w;
+  const float det = dudx * dvdy - dvdx * dudy;
+  Foot f;
+  f.a = dudx * dudx + dudy * dudy;
+  f.b = dudx * dvdx + dudy * dvdy;
+  f.c = dvdx * dvdx + dvdy * dvdy;
+  const float hm = 0.5f * (f.a - f.c);
+  const float dv = hm * hm + f.b * f.b;
+  const float disc = dv >= 0x1p-126f ? dv * rsqrt_c(dv) : 0.0f;   // contract sqrt (subnormal -> 0)
+  f.lam = 0.5f * (f.a + f.c) + disc;
+  f.P = fabsf(det);
+  return f;
+}
+__device__ __forceinline__ bool s1_valid(const Foot& f) { return f.P >= 0x1p-64f && f.P < 0x1p64f && f.lam < 0x1p126f; }
+__device__ __forceinline__ bool uv_ok(float4 uvm) {
+  return (__float_as_uint(uvm.w) & 1u) != 0 && fabsf(uvm.x) <= 0x1p24f && fabsf(uvm.y) <= 0x1p24f;
+}
+// unnormalised direction d towards the light, |d|^2 and n.d
+__device__ __forceinline__ void light_dir(const glint_light& lt, float4 pos, float nx, float ny, float nz, float& dx,
+                                          float& dy, float& dz, float& d2, float& nd) {
+  if (lt.kind == 0) { dx = lt.pos_or_dir[0] - pos.x; dy = lt.pos_or_dir[1] - pos.y; dz = lt.pos_or_dir[2] - pos.z; }
+  else { dx = lt.pos_or_dir[0]; dy = lt.pos_or_dir[1]; dz = lt.pos_or_dir[2]; }
+  d2 = dot3(dx, dy, dz, dx, dy, dz);
+  nd = dot3(nx, ny, nz, dx, dy, dz);
+}
+__device__ __forceinline__ bool light_active(float ni, float nd, float d2) {
+  return ni > 0.0f && nd > 0.0f && d2 >= 0x1p-126f && d2 <= 0x1p120f;
+}
+__device__ __forceinline__ void view_dir(const glint_scene& sc, float4 pos, float& wix, float& wiy, float& wiz) {
+  if (sc.view_kind == 0) { wix = sc.view[0] - pos.x; wiy = sc.view[1] - pos.y; wiz = sc.view[2] - pos.z; }
+  else { wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2]; }
+  normalize3(wix, wiy, wiz);
+}
+
+// ---------------------------------------------------------------------------
+// S9 radiance shell (Eq. 1-2; readings R-21, R-27), fp64 from the
+// raw fp32 inputs (normal, position, view, light): no fp32 rounding of a
+// cosine or of view - pos reaches the radiance, so grazing pixels meet the
+// 1e-4 tolerance too. Runs only in the warp-uniform "some lane has C > 0"
+// block; rcp / rsqrt from the MUFU double-precision seeds plus Newton steps
+// (relative error ~1e-15, tolerance path only).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double rcp_d(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+__device__ __forceinline__ double rsqrt_d(double x) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double hx = 0.5 * x;
+  y = y * fma(-hx, y * y, 1.5);
+  return y * fma(-hx, y * y, 1.5);
+}
+__device__ __forceinline__ double dot3d(double ax, double ay, double az, double bx, double by, double bz) {
+  return fma(az, bz, fma(ay, by, ax * bx));
+}
+// Smith Lambda in the local frame: GGX exact q/(2(1+sqrt(1+q))), q = s/wz^2,
+// written s/(2 wz (wz + sqrt(wz^2 + s))) (wz > 0); Beckmann Walter 2007 rational
+__device__ __forceinline__ double smith_lambda_d(int kind, double ax2, double ay2, double wx, double wy, double wz) {
+  const double s = fma(ax2, wx * wx, ay2 * (wy * wy));
+  if (!(s > 0.0)) return 0.0;
   if (kind == 0) {
-    const float q = __fdividef(s, wz * wz);
-    const float r1 = 1.0f + q;
-    return __fdividef(q, 2.0f * (1.0f + r1 * rsqrtf(r1)));
+    const double t = fma(wz, wz, s);
+    const double sq = t * rsqrt_d(t);
+    return s * rcp_d(2.0 * wz * (wz + sq));
   }
-  const float a = wz * rsqrtf(s);
-  if (a >= 1.6f) return 0.0f;
-  return __fdividef(__fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f), a * __fmaf_rn(2.181f, a, 3.535f));
+  const double a = wz * rsqrt_d(s);
+  if (a >= 1.6) return 0.0;
+  return fma(a, fma(0.396, a, -1.259), 1.0) * rcp_d(a * fma(2.181, a, 3.535));
+}
+// L += F G2 D_P E / (4 n.wi) of one light for the pixel (fp64 -> fp32 once
+// per channel); D_P = C / (pi ax ay R N P) (Eq. 3-4, R-20). Adds nothing when
+// C = 0 or an fp64 cosine is not > 0 (DESIGN.md §4.3 S9).
+__device__ __forceinline__ void radiance_shell(const glint_scene& sc, const glint_light& lt, float4 nrm, float4 pos,
+                                               float ax, float ay, float R, float N, float P, float C, float3& rgb) {
+  if (!(C > 0.0f)) return;
+  double nx = nrm.x, ny = nrm.y, nz = nrm.z;
+  {
+    const double in = rsqrt_d(dot3d(nx, ny, nz, nx, ny, nz));
+    nx *= in; ny *= in; nz *= in;
+  }
+  const double sgn = copysign(1.0, nz);
+  const double oa = -rcp_d(sgn + nz);
+  const double ob = nx * ny * oa;
+  const double tx = fma(sgn * nx, nx * oa, 1.0), ty = sgn * ob, tz = -sgn * nx;
+  const double bx = ob, by = fma(ny, ny * oa, sgn), bz = -ny;
+  double wix, wiy, wiz;
+  if (sc.view_kind == 0) {
+    wix = (double)sc.view[0] - (double)pos.x; wiy = (double)sc.view[1] - (double)pos.y; wiz = (double)sc.view[2] - (double)pos.z;
+  } else {
+    wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2];
+  }
+  {
+    const double in = rsqrt_d(dot3d(wix, wiy, wiz, wix, wiy, wiz));
+    wix *= in; wiy *= in; wiz *= in;
+  }
+  double wox, woy, woz, E = 1.0;
+  if (lt.kind == 0) {
+    wox = (double)lt.pos_or_dir[0] - (double)pos.x; woy = (double)lt.pos_or_dir[1] - (double)pos.y;
+    woz = (double)lt.pos_or_dir[2] - (double)pos.z;
+  } else {
+    wox = lt.pos_or_dir[0]; woy = lt.pos_or_dir[1]; woz = lt.pos_or_dir[2];
+  }
+  {
+    const double d2 = dot3d(wox, woy, woz, wox, woy, woz);
+    const double in = rsqrt_d(d2);
+    if (lt.kind == 0) E = in * in;   // 1 / d^2
+    wox *= in; woy *= in; woz *= in;
+  }
+  const double ci = dot3d(nx, ny, nz, wix, wiy, wiz), co = dot3d(nx, ny, nz, wox, woy, woz);
+  if (!(ci > 0.0) || !(co > 0.0)) return;
+  double hx = wix + wox, hy = wiy + woy, hz = wiz + woz;
+  {
+    const double in = rsqrt_d(dot3d(hx, hy, hz, hx, hy, hz));
+    hx *= in; hy *= in; hz *= in;
+  }
+  const double cih = dot3d(wix, wiy, wiz, hx, hy, hz);
+  const double ax2 = (double)ax * ax, ay2 = (double)ay * ay;
+  const double li = smith_lambda_d(sc.ndf_kind, ax2, ay2, dot3d(wix, wiy, wiz, tx, ty, tz), dot3d(wix, wiy, wiz, bx, by, bz), ci);
+  const double lo = smith_lambda_d(sc.ndf_kind, ax2, ay2, dot3d(wox, woy, woz, tx, ty, tz), dot3d(wox, woy, woz, bx, by, bz), co);
+  // G2 D_P E / (4 n.wi) = C E / ((1 + Li + Lo) pi ax ay R N P 4 n.wi)
+  const double den = (1.0 + li + lo) * (3.141592653589793 * (double)ax * (double)ay * (double)R * (double)N * (double)P) *
+                     (4.0 * ci);
+  const double k = (double)C * E * rcp_d(den);
+  const double om = 1.0 - cih;
+  const double om2 = om * om;
+  const double om5 = om2 * om2 * om;
+  rgb.x += (float)(fma(1.0 - (double)sc.f0[0], om5, (double)sc.f0[0]) * (k * (double)lt.intensity[0]));
+  rgb.y += (float)(fma(1.0 - (double)sc.f0[1], om5, (double)sc.f0[1]) * (k * (double)lt.intensity[1]));
+  rgb.z += (float)(fma(1.0 - (double)sc.f0[2], om5, (double)sc.f0[2]) * (k * (double)lt.intensity[2]));
 }
 
 // shared tables at namespace scope: fixed shared-window offsets, so the
@@ -217,31 +348,20 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   uint32_t flags = 0;
   const uint32_t meta = __float_as_uint(uvm.w);
   const float u = uvm.x, v = uvm.y;
-  bool ok = (meta & 1u) != 0;
-  if (!ok) flags = GLINT_FLAG_INVALID;
-  if (ok && !(fabsf(u) <= 0x1p24f && fabsf(v) <= 0x1p24f)) {
-    flags = GLINT_FLAG_INVALID | GLINT_FLAG_UV_RANGE;
-    ok = false;
-  }
+  bool ok = uv_ok(uvm);
+  if (!ok) flags = (meta & 1u) ? (GLINT_FLAG_INVALID | GLINT_FLAG_UV_RANGE) : GLINT_FLAG_INVALID;
   // ---------------- S1: footprint (R-7, R-8)
   float P = 0.0f, r = 0.0f, psi = 0.0f;
   float zex = 1.0f, zey = 0.0f, zsmax = 0.0f;   // MODE 3: major axis, sigma_max (R-32)
   if (ok) {
-    const float dudx = duv.x, dvdx = duv.y, dudy = duv.z, dvdy = duv.w;
-    const float det = dudx * dvdy - dvdx * dudy;
-    const float a = dudx * dudx + dudy * dudy;
-    const float b = dudx * dvdx + dudy * dvdy;
-    const float c = dvdx * dvdx + dvdy * dvdy;
-    const float hm = 0.5f * (a - c);
-    const float dv = hm * hm + b * b;
-    const float disc = dv >= 0x1p-126f ? dv * rsqrt_c(dv) : 0.0f;   // contract sqrt (subnormal -> 0)
-    const float lam = 0.5f * (a + c) + disc;
-    P = fabsf(det);
+    const Foot f = s1_moments(duv);
+    const float a = f.a, b = f.b, c = f.c, lam = f.lam;
+    P = f.P;
     r = lam * rcp_c(P);
     const float at = atan2_turns(2.0f * b, a - c);
     psi = at < 0.0f ? at + 1.0f : at;
     if (psi >= 1.0f) psi = 0.0f;
-    if (!(P >= 0x1p-64f && P < 0x1p64f && lam < 0x1p126f)) {   // R-25, R-30b
+    if (!s1_valid(f)) {   // R-25, R-30b
       flags = GLINT_FLAG_DEGENERATE;
       ok = false;
     }
@@ -360,27 +480,16 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   const float tx = 1.0f + sgn * ((nx * nx) * oa), ty = sgn * ob, tz = -(sgn * nx);
   const float bx = ob, by = sgn + (ny * ny) * oa, bz = -ny;
   float wix, wiy, wiz;
-  if (sc.view_kind == 0) { wix = sc.view[0] - pos.x; wiy = sc.view[1] - pos.y; wiz = sc.view[2] - pos.z; }
-  else { wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2]; }
-  normalize3(wix, wiy, wiz);
+  view_dir(sc, pos, wix, wiy, wiz);
   const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
   const float iax = rcp_c(ax), iay = rcp_c(ay);
-  // radiance-path constants (tolerance path: fast intrinsics allowed)
-  // radiance-path constants, computed on first use (most pixels receive no
-  // glint from any light: C = 0)
-  const float ax2 = ax * ax, ay2 = ay * ay;
-  float lam_i = 0.0f, dp_scale = 0.0f, rad_scale = 0.0f;
-  bool have_rad = false;
   float3 rgb = make_float3(0.0f, 0.0f, 0.0f);
 
   for (int l = 0; l < L; ++l) {
     const glint_light& lt = sc.lights[l];
     // ---------------- S5: light direction d (unnormalised), activity, h, p
-    float dx, dy, dz;
-    if (lt.kind == 0) { dx = lt.pos_or_dir[0] - pos.x; dy = lt.pos_or_dir[1] - pos.y; dz = lt.pos_or_dir[2] - pos.z; }
-    else { dx = lt.pos_or_dir[0]; dy = lt.pos_or_dir[1]; dz = lt.pos_or_dir[2]; }
-    const float d2 = dot3(dx, dy, dz, dx, dy, dz);
-    const float nd = dot3(nx, ny, nz, dx, dy, dz);    // sign of n.wo
+    float dx, dy, dz, d2, nd;   // nd: sign of n.wo
+    light_dir(lt, pos, nx, ny, nz, dx, dy, dz, d2, nd);
     glint_debug_rec* rc = DEBUG ? rec + l : nullptr;
     if (DEBUG) {
       uint32_t* w = reinterpret_cast<uint32_t*>(rc);
@@ -390,7 +499,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       for (int q = 0; q < 12; ++q) { rc->lx[q] = (int32_t)dlx[q]; rc->ly[q] = (int32_t)dly[q]; }
     }
     // light below the horizon (R-27); |d|^2 a normal float (R-27b)
-    if (!(ni > 0.0f && nd > 0.0f && d2 >= 0x1p-126f && d2 <= 0x1p120f)) continue;
+    if (!light_active(ni, nd, d2)) continue;
     if (DEBUG) rc->light_active = 1u;
     // h = normalize(|d| wi + d)  (proportional to wi + wo, one division less)
     const float dl = d2 * rsqrt_c(d2);
@@ -524,7 +633,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
           for (int jn = 0; jn < 4; ++jn) {
             uint32_t y = hC + kaC[jn];
-            y ^= __funnelshift_r(y, y, 15);
+            y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
             y *= 0x846ca68bU;
             const uint32_t s16 = y >> 16;
             const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
@@ -562,7 +671,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 #pragma unroll
         for (int jn = 0; jn < 4; ++jn) {
           uint32_t y = hsC[i * 3 + k] + kaC[jn];        // (hs + ka) * C1
-          y ^= __funnelshift_r(y, y, 15);           // xor-rotate (R-23b)
+          y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);   // bijective xor-rotate (R-23b)
           y *= 0x846ca68bU;                              // y: gate bits 9..31
           const uint32_t s16 = y >> 16;                  // h = y ^ (y >> 16): quantile bits 2..13
           const float z = *reinterpret_cast<const float*>(reinterpret_cast<const char*>(sZ) + ((y ^ s16) & 0x3FFCu));
@@ -573,34 +682,16 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       }
     }
     const float C = __fmaf_rn(vj[3], A[3], __fmaf_rn(vj[2], A[2], __fmaf_rn(vj[1], A[1], vj[0] * A[0])));
-    if (DEBUG || (C > 0.0f && !have_rad)) {
-      lam_i = smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wix, wiy, wiz, tx, ty, tz), dot3(wix, wiy, wiz, bx, by, bz), ni);
-      // D_P / (4 n.wi) = C D(n) / (R N P 4 n.wi), D(n) = 1/(pi ax ay)  (Eq. 2-4, R-20)
-      dp_scale = __fdividef(1.0f, 3.14159265358979f * ax * ay * R * N * P);
-      rad_scale = __fdividef(dp_scale, 4.0f * ni);
-      have_rad = true;
+    if (DEBUG) {
+      rc->C = C;
+      rc->Dp = C > 0.0f ? (float)((double)C * rcp_d(3.141592653589793 * (double)ax * (double)ay * (double)R * (double)N *
+                                                    (double)P))
+                        : 0.0f;
     }
-    if (DEBUG) { rc->C = C; rc->Dp = C > 0.0f ? C * dp_scale : 0.0f; (void)dhs; }
-    // ---------------- S8/S9: D_P and radiance (Eq. 1-3), tolerance path
-    // warp-uniform: lanes with C = 0 add exactly 0 (their D_P term is 0), so
-    // the radiance block runs without per-lane divergence
-    if (DEBUG ? (C > 0.0f) : __any_sync(am, C > 0.0f)) {
-      const float idl = __fdividef(1.0f, dl);
-      const float wox = dx * idl, woy = dy * idl, woz = dz * idl;
-      const float E = (lt.kind == 0) ? __fdividef(1.0f, d2) : 1.0f;
-      const float G2 = __fdividef(1.0f, 1.0f + lam_i + smith_lambda(sc.ndf_kind, ax2, ay2, dot3(wox, woy, woz, tx, ty, tz),
-                                                                   dot3(wox, woy, woz, bx, by, bz), nd * idl));
-      const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
-      const float om = 1.0f - cih;
-      const float om2 = om * om;
-      const float om5 = om2 * om2 * om;
-      // irradiance I E first: E = 1/d^2 can be ~1e-36 against I ~ 1e36, and
-      // G2 C rad_scale E alone would go subnormal (lost bits)
-      const float kk = G2 * C * rad_scale;
-      rgb.x += (sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk * (lt.intensity[0] * E);
-      rgb.y += (sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk * (lt.intensity[1] * E);
-      rgb.z += (sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk * (lt.intensity[2] * E);
-    }
+    // ---------------- S8/S9: D_P and radiance (Eq. 1-3), fp64 shell.
+    // Warp-uniform: lanes with C = 0 add exactly nothing (the shell returns
+    // at once), so the block runs without per-lane divergence
+    if (DEBUG ? (C > 0.0f) : __any_sync(am, C > 0.0f)) radiance_shell(sc, lt, nrm, pos, ax, ay, R, N, P, C, rgb);
   }
   if (DEBUG) for (int l = 0; l < L; ++l) rec[l].flags = flags;
   __stcs(outp, make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(flags)));
@@ -783,6 +874,46 @@ cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t s
     default:
       return tma ? launch_t<false, true, 0>(prm, grid, stream, pdl) : launch_t<false, false, 0>(prm, grid, stream, pdl);
   }
+}
+
+// ---------------------------------------------------------------------------
+// glint_count_active: the (pixel, light) pairs whose S5-S9 work glint_eval
+// does, with the kernel's own decision functions (uv_ok, s1_moments/s1_valid,
+// view_dir, light_dir/light_active). Grid-stride, one warp-reduced atomic per
+// warp into the caller's counter.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) count_active_kernel(const float4* __restrict__ duv, const float4* __restrict__ uvm,
+                                                           const float4* __restrict__ nrm, const float4* __restrict__ pos,
+                                                           int32_t width, int64_t n_pix, int64_t pitch,
+                                                           const glint_scene sc, unsigned long long* count) {
+  unsigned long long c = 0;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n_pix; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = idx / width, x = idx - y * width;
+    const int64_t gi = y * pitch + x;
+    const float4 u = uvm[gi];
+    if (!uv_ok(u)) continue;
+    if (!s1_valid(s1_moments(duv[gi]))) continue;
+    const float4 nr = nrm[gi], ps = pos[gi];
+    float nx = nr.x, ny = nr.y, nz = nr.z;
+    normalize3(nx, ny, nz);
+    float wix, wiy, wiz;
+    view_dir(sc, ps, wix, wiy, wiz);
+    const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
+    for (int l = 0; l < sc.n_lights; ++l) {
+      float dx, dy, dz, d2, nd;
+      light_dir(sc.lights[l], ps, nx, ny, nz, dx, dy, dz, d2, nd);
+      c += light_active(ni, nd, d2) ? 1ull : 0ull;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+cudaError_t launch_count_active(const float4* duv, const float4* uvm, const float4* nrm, const float4* pos, int32_t width,
+                                int32_t height, int64_t pitch, const glint_scene& sc, unsigned long long* count,
+                                int grid, cudaStream_t stream) {
+  count_active_kernel<<<grid, 256, 0, stream>>>(duv, uvm, nrm, pos, width, (int64_t)width * height, pitch, sc, count);
+  return cudaGetLastError();
 }
 
 cudaError_t occupancy_blocks_per_sm(int* out) {

@@ -26,6 +26,7 @@ constexpr int kTile = kBlock * kPPT;            // pixels per tile
 constexpr int kStages = GLINT_STAGES;           // G-buffer tile ring (full/empty mbarrier pairs)
 constexpr int kWarps = kBlock / 32;
 constexpr int kSchedSlots = 1024;               // per-context ring of per-launch scheduler counters
+constexpr int kCaptureSlots = 4096;             // per-context pool for graph-captured launches (never recycled)
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
 constexpr size_t kSmemTables = 256;    // dynamic part: table + kStages mbarriers, tile ids, counters (padded)
@@ -54,5 +55,8 @@ struct KParams {
 
 cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream, bool pdl = false);
 cudaError_t occupancy_blocks_per_sm(int* out);
+cudaError_t launch_count_active(const float4* duv, const float4* uvm, const float4* nrm, const float4* pos, int32_t width,
+                                int32_t height, int64_t pitch, const glint_scene& sc, unsigned long long* count,
+                                int grid, cudaStream_t stream);
 
 }  // namespace glint

@@ -27,7 +27,7 @@ def test_exports_match_header(glib):
     L = glib.lib()
     for name in declared:
         assert hasattr(L, name)
-    assert glib.version() == 10000
+    assert glib.version() == 20000
     assert glib.strerror(-1) == "invalid argument"
 
 
@@ -55,7 +55,7 @@ def test_argument_errors_without_gpu(glib):
 def test_scene_struct_layout(glib):
     assert C.sizeof(glib._lib.glint_light) == 32
     assert C.sizeof(glib._lib.glint_scene) == 64 + 16 * 32
-    assert C.sizeof(glib._lib.glint_gbuffer) == 5 * 8 + 4 + 4 + 8
+    assert C.sizeof(glib._lib.glint_gbuffer) == 5 * 8 + 4 + 4 + 8 + 4 + 4   # + tile origin (x0, y0)
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(),
@@ -150,3 +150,43 @@ def test_batch_alias_rule_against_brute_force(glib):
             assert refused == truth, (P1, P2, w1, h1, w2, h2, o1 - base, o2 - base)
         else:
             assert refused or not truth, (P1, P2, w1, h1, w2, h2, o1 - base, o2 - base)
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(),
+                    reason="fake, never dereferenced addresses are safe only where the device check fails")
+def test_tile_origins_in_one_output_alias_rule_without_gpu(glib):
+    """Row bands of one frame written into ONE full-frame output through their
+    tile origins (glint.h x0, y0; SURVEY 8e sharding): disjoint bands pass the
+    batch's alias rule, overlapping bands are refused, a negative origin is
+    invalid and an origin past 2^40 float4 is refused as too large -- all
+    before the context or device is touched."""
+    import torch
+    L = glib.lib()
+    m = glib._lib
+    W, Hb, pitch = 64, 8, 64
+    plane = pitch * Hb * 16
+    sc = m.scene_struct(__import__("paper_2306_05051_b200.synth", fromlist=["x"]).SceneParams())
+    fake = C.c_void_p(0x1000)
+
+    def band(base, y0, x0=0):
+        g = m.glint_gbuffer()
+        g.duv, g.uvm, g.nrm, g.pos, g.mat = [base + k * plane for k in range(5)]
+        g.width, g.height, g.pitch, g.x0, g.y0 = W, Hb, pitch, x0, y0
+        return g
+
+    out = 0x70000000
+    S = (m.glint_scene * 2)(sc, sc)
+    Q = (C.c_int64 * 2)(W, W)
+    P = (C.c_void_p * 2)(out, out)                   # the same full-frame output for both bands
+
+    def run(g0, g1):
+        return L.glint_eval_batch(fake, 2, (m.glint_gbuffer * 2)(g0, g1), S, P, Q, None)
+
+    rc = run(band(0x10000000, 0), band(0x20000000, Hb))            # rows 0-7 and 8-15
+    assert rc in (m.GLINT_ECUDA, m.GLINT_EDEVICE)
+    assert run(band(0x10000000, 0), band(0x20000000, Hb - 1)) == m.GLINT_EALIAS   # one shared row
+    assert run(band(0x10000000, 0), band(0x20000000, 3)) == m.GLINT_EALIAS
+    assert run(band(0x10000000, 0, x0=-1), band(0x20000000, Hb)) == m.GLINT_EINVAL
+    G = (m.glint_gbuffer * 2)(band(0x10000000, 0), band(0x20000000, 64))
+    Qbig = (C.c_int64 * 2)(W, 2 ** 34)                                  # (64 + 8) rows x 2^34 >= 2^40
+    assert L.glint_eval_batch(fake, 2, G, S, P, Qbig, None) == m.GLINT_ELIMIT

@@ -44,11 +44,12 @@ import pytest  # noqa: E402
 
 @pytest.mark.gpu
 def test_our_arm_json_line_on_the_gpu():
-    """Our arm on one B200 (default C2 workload, a short run): one JSON line
+    """Our arm on one B200 (the C2 workload, a short run): one JSON line
     with every key of the driver's contract, the roofline and cpu_baseline
     objects, the e2e object through the host-buffer batch entry, the launch
-    count of the timed region (10 frames per step), clocks sampled during it."""
-    cmd = [sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--e2e-steps", "2"]
+    count of the timed region (10 frames per step), clocks sampled during it,
+    evals counted as active pairs (<= the replicated valid x lights count)."""
+    cmd = [sys.executable, "bench.py", "--config", "C2", "--steps", "3", "--warmup", "3", "--e2e-steps", "2"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -57,9 +58,12 @@ def test_our_arm_json_line_on_the_gpu():
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
-    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["scaling"] == "weak"
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["scaling"] == "strong"
     assert d["value"] > 1e9 and d["higher_is_better"] is True and d["vs_baseline"] is None
-    assert d["config"]["workload"].startswith("C2") and d["config"]["launches_per_step"] == 10
+    cf = d["config"]
+    assert cf["workload"].startswith("C2") and cf["launches_per_step_per_rank"] == 10
+    assert 0 < cf["evals_per_step_per_rank"] <= cf["evals_replicated_per_step_per_rank"]
+    assert cf["verified"].startswith("all 10 frames written")
     assert d["gpu_launches"] == 30
     ro = d["roofline"]
     assert ro["bound"] == "alu" and 0 < ro["frac"] < 1 and ro["peak"] > 0
@@ -69,8 +73,8 @@ def test_our_arm_json_line_on_the_gpu():
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["sample"] and cb["value"] > 0
     e = d["e2e"]
     assert e["api"].startswith("glint_eval_host_batch") and e["value"] > 0
-    assert e["h2d_bytes_per_step"] == d["config"]["pixels_per_step"] * 80
-    assert e["d2h_bytes_per_step"] == d["config"]["pixels_per_step"] * 16
+    assert e["h2d_bytes_per_step"] == cf["pixels_per_step_per_rank"] * 80
+    assert e["d2h_bytes_per_step"] == cf["pixels_per_step_per_rank"] * 16
     c = d["clocks"]
     assert isinstance(c["reasons"], list) and "samples" in c
     if c["samples"]:      # a 3-step region is short: NVML may not have sampled it

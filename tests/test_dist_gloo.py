@@ -66,3 +66,85 @@ def test_gloo_world2():
     assert res0[3] == list(range(10))                 # rank 0 has every frame
     for f, v in res0[4].items():
         assert v == f * 10 + (f % 2)                  # frame f came from rank f % 2
+
+
+def _shade_tile_oracle(f, y0, y1, W=64, H=48):
+    """The test's stand-in for a rank's kernel: the oracle on one tile of a
+    small C2 frame (elevation by frame), as an (rows, W, 4) float32 image
+    (RGB rounded to fp32, flag bits in .w)."""
+    import numpy as np
+    import oracle
+    from paper_2306_05051_b200 import synth
+    fr = synth.c2(15 + 20 * f, width=W, height=H, window=(y0, y1, 0, W))
+    rgb, fl, _ = oracle.eval(fr.gbuf, fr.scene)
+    img = np.zeros((y1 - y0, W, 4), np.float32)
+    img[..., :3] = rgb.reshape(y1 - y0, W, 3).astype(np.float32)
+    img[..., 3] = fl.reshape(y1 - y0, W).view(np.float32)
+    return torch.from_numpy(img)
+
+
+def _tile_worker(rank, world, port, n_frames, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
+                      LOCAL_RANK=str(rank))
+    try:
+        r, w, _ = D.init("gloo")
+        H, W = 48, 64
+        tiles = D.plan_tiles(n_frames, H, w, band_rows=16)
+        g = D.TileGather(tiles, r, w, full=[torch.full((H, W, 4), float("nan")) for _ in range(n_frames)]
+                         if r == 0 else None)
+        local = {}
+        for i in g.mine:
+            f, y0, y1 = tiles[i]
+            img = _shade_tile_oracle(f, y0, y1)
+            if r == 0:
+                g.full[f][y0:y1] = img           # rank 0 shades in place
+            else:
+                local[i] = img
+        for wk in g.run(local):
+            wk.wait()
+        D.barrier()
+        q.put((r, [t.numpy().copy() for t in g.full] if r == 0 else None, tiles))
+        dist.destroy_process_group()
+    except Exception as e:   # report instead of hanging the parent
+        q.put((rank, repr(e), None))
+
+
+@pytest.mark.parametrize("n_frames", [1, 3])
+def test_gloo_tile_gather_assembles_the_single_rank_image(n_frames):
+    """SURVEY 8e at world size 2 on CPU: one frame cut into 16-row bands (C2 /
+    C3-style row-band sharding, the last band on the second rank) or three
+    whole frames (C4 / C5-style frame sharding), each tile shaded by its rank
+    (the oracle stands in for the kernel) and gathered to rank 0 by the
+    per-tile send/recv rounds of dist.TileGather: rank 0's assembled frames
+    equal the whole frames shaded in one process, bit for bit."""
+    import numpy as np
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_tile_worker, args=(r, 2, port, n_frames, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = {r: (full, tiles) for r, full, tiles in (q.get(timeout=300) for _ in ps)}
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full, tiles = res[0]
+    assert not isinstance(full, str), full
+    assert len(tiles) == (3 if n_frames == 1 else 3)            # 48 rows / 16 = 3 bands, or 3 frames
+    assert {i % 2 for i in range(len(tiles))} == {0, 1}         # both ranks shaded something
+    for f in range(n_frames):
+        ref = _shade_tile_oracle(f, 0, 48).numpy()
+        assert np.array_equal(full[f].view(np.uint32), ref.view(np.uint32)), f
+
+
+def test_plan_tiles_partitions_every_row_once():
+    for n_frames, H, world in ((1, 2160, 8), (10, 1080, 8), (10, 1080, 1), (64, 2160, 8), (8, 2160, 3), (1, 37, 4)):
+        tiles = D.plan_tiles(n_frames, H, world)
+        rows = {}
+        for f, y0, y1 in tiles:
+            for y in range(y0, y1):
+                assert (f, y) not in rows
+                rows[(f, y)] = 1
+        assert len(rows) == n_frames * H
+        per_rank = [len(D.shard(tiles, r, world)) for r in range(world)]
+        assert max(per_rank) - min(per_rank) <= 1
