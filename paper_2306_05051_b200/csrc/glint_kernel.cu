@@ -229,105 +229,139 @@ __device__ __forceinline__ void view_dir(const glint_scene& sc, float4 pos, floa
 }
 
 // ---------------------------------------------------------------------------
-// S9 radiance shell (Eq. 1-2; readings R-21, R-27), fp64 from the
-// raw fp32 inputs (normal, position, view, light): no fp32 rounding of a
-// cosine or of view - pos reaches the radiance, so grazing pixels meet the
-// 1e-4 tolerance too. Runs only in the warp-uniform "some lane has C > 0"
-// block; rcp / rsqrt from the MUFU double-precision seeds plus Newton steps
-// (relative error ~1e-15, tolerance path only).
+// S9 radiance shell (Eq. 1-2; readings R-21, R-27), tolerance
+// path (1e-4 relative against the oracle's fp64). Two tiers, chosen per
+// lane by the same rule in the production and DEBUG kernels (so both give the
+// same bits):
+//  * radiance_shell32, fp32 with MUFU rsqrt / reciprocals, for the
+//    well-conditioned lanes: both shading cosines >= 2^-6 and every f0 >=
+//    2^-10 (DESIGN.md §4.1 error budget: <= ~4e-5 worst case, 2e-6 measured);
+//  * radiance_shell64 for the rest (grazing view or light, tiny f0, factors
+//    out of fp32's comfortable range): the cosines, the irradiance and
+//    Schlick's 1 - w_i.h in fp64 from the raw fp32 inputs.
+// Both run only in the warp-uniform "some lane has C > 0" block.
 // ---------------------------------------------------------------------------
+// rcp / rsqrt from the MUFU double-precision seeds (rcp.approx / rsqrt.approx
+// .f64) plus one Newton step: relative error far below the tolerance
 __device__ __forceinline__ double rcp_d(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  return fma(r, fma(-x, r, 1.0), r);     // one Newton step
 }
 __device__ __forceinline__ double rsqrt_d(double x) {
   double y;
   asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double hx = 0.5 * x;
-  y = y * fma(-hx, y * y, 1.5);
-  return y * fma(-hx, y * y, 1.5);
+  return y * fma(-0.5 * x, y * y, 1.5);  // one Newton step
 }
 __device__ __forceinline__ double dot3d(double ax, double ay, double az, double bx, double by, double bz) {
   return fma(az, bz, fma(ay, by, ax * bx));
 }
-// Smith Lambda in the local frame: GGX exact q/(2(1+sqrt(1+q))), q = s/wz^2,
-// written s/(2 wz (wz + sqrt(wz^2 + s))) (wz > 0); Beckmann Walter 2007 rational
-__device__ __forceinline__ double smith_lambda_d(int kind, double ax2, double ay2, double wx, double wy, double wz) {
-  const double s = fma(ax2, wx * wx, ay2 * (wy * wy));
-  if (!(s > 0.0)) return 0.0;
+// Smith G2 = 1 / (1 + Lambda(w_i) + Lambda(w_o)) (R-21) as one fraction,
+// Lambda = num / den per direction (num = 0, den = 1 for Lambda = 0): GGX
+// exact Lambda = s / (2 c (c + sqrt(c^2 + s))), Beckmann Walter 2007
+// rational in a = c / sqrt(s) (0 from a >= 1.6). s = ax^2 wx^2 + ay^2 wy^2
+// (tangential part), c = n.w (fp64, relative accuracy at grazing).
+__device__ __forceinline__ void lambda_frac(int kind, double s, double c, double& num, double& den) {
+  num = 0.0;
+  den = 1.0;
+  if (!(s > 0.0)) return;
   if (kind == 0) {
-    const double t = fma(wz, wz, s);
-    const double sq = t * rsqrt_d(t);
-    return s * rcp_d(2.0 * wz * (wz + sq));
+    const double t = fma(c, c, s);
+    num = s;
+    den = 2.0 * c * (c + t * rsqrt_d(t));
+    return;
   }
-  const double a = wz * rsqrt_d(s);
-  if (a >= 1.6) return 0.0;
-  return fma(a, fma(0.396, a, -1.259), 1.0) * rcp_d(a * fma(2.181, a, 3.535));
+  const double a = c * rsqrt_d(s);
+  if (a >= 1.6) return;
+  num = fma(a, fma(0.396, a, -1.259), 1.0);
+  den = a * fma(2.181, a, 3.535);
 }
-// L += F G2 D_P E / (4 n.wi) of one light for the pixel (fp64 -> fp32 once
-// per channel); D_P = C / (pi ax ay R N P) (Eq. 3-4, R-20). Adds nothing when
-// C = 0 or an fp64 cosine is not > 0 (DESIGN.md §4.3 S9).
-__device__ __forceinline__ void radiance_shell(const glint_scene& sc, const glint_light& lt, float4 nrm, float4 pos,
-                                               float ax, float ay, float R, float N, float P, float C, float3& rgb) {
-  if (!(C > 0.0f)) return;
-  double nx = nrm.x, ny = nrm.y, nz = nrm.z;
-  {
-    const double in = rsqrt_d(dot3d(nx, ny, nz, nx, ny, nz));
-    nx *= in; ny *= in; nz *= in;
-  }
-  const double sgn = copysign(1.0, nz);
-  const double oa = -rcp_d(sgn + nz);
-  const double ob = nx * ny * oa;
-  const double tx = fma(sgn * nx, nx * oa, 1.0), ty = sgn * ob, tz = -sgn * nx;
-  const double bx = ob, by = fma(ny, ny * oa, sgn), bz = -ny;
-  double wix, wiy, wiz;
-  if (sc.view_kind == 0) {
-    wix = (double)sc.view[0] - (double)pos.x; wiy = (double)sc.view[1] - (double)pos.y; wiz = (double)sc.view[2] - (double)pos.z;
-  } else {
-    wix = sc.view[0]; wiy = sc.view[1]; wiz = sc.view[2];
-  }
-  {
-    const double in = rsqrt_d(dot3d(wix, wiy, wiz, wix, wiy, wiz));
-    wix *= in; wiy *= in; wiz *= in;
-  }
-  double wox, woy, woz, E = 1.0;
-  if (lt.kind == 0) {
-    wox = (double)lt.pos_or_dir[0] - (double)pos.x; woy = (double)lt.pos_or_dir[1] - (double)pos.y;
-    woz = (double)lt.pos_or_dir[2] - (double)pos.z;
-  } else {
-    wox = lt.pos_or_dir[0]; woy = lt.pos_or_dir[1]; woz = lt.pos_or_dir[2];
-  }
-  {
-    const double d2 = dot3d(wox, woy, woz, wox, woy, woz);
-    const double in = rsqrt_d(d2);
-    if (lt.kind == 0) E = in * in;   // 1 / d^2
-    wox *= in; woy *= in; woz *= in;
-  }
-  const double ci = dot3d(nx, ny, nz, wix, wiy, wiz), co = dot3d(nx, ny, nz, wox, woy, woz);
-  if (!(ci > 0.0) || !(co > 0.0)) return;
-  double hx = wix + wox, hy = wiy + woy, hz = wiz + woz;
-  {
-    const double in = rsqrt_d(dot3d(hx, hy, hz, hx, hy, hz));
-    hx *= in; hy *= in; hz *= in;
-  }
-  const double cih = dot3d(wix, wiy, wiz, hx, hy, hz);
-  const double ax2 = (double)ax * ax, ay2 = (double)ay * ay;
-  const double li = smith_lambda_d(sc.ndf_kind, ax2, ay2, dot3d(wix, wiy, wiz, tx, ty, tz), dot3d(wix, wiy, wiz, bx, by, bz), ci);
-  const double lo = smith_lambda_d(sc.ndf_kind, ax2, ay2, dot3d(wox, woy, woz, tx, ty, tz), dot3d(wox, woy, woz, bx, by, bz), co);
-  // G2 D_P E / (4 n.wi) = C E / ((1 + Li + Lo) pi ax ay R N P 4 n.wi)
-  const double den = (1.0 + li + lo) * (3.141592653589793 * (double)ax * (double)ay * (double)R * (double)N * (double)P) *
-                     (4.0 * ci);
-  const double k = (double)C * E * rcp_d(den);
+// F G2 D_P E / (4 n.wi) of one light for the pixel (Eq. 1-4, R-20, R-21):
+// the cosines n.wi, n.wo, the irradiance E and Schlick's 1 - w_i.h in fp64
+// from the raw fp32 inputs (exact differences view - pos, light - pos and
+// exact products: relative accuracy at grazing and near retro-reflection);
+// the tangential parts of w_i, w_o in the fp32 frame of the decision path
+// (they enter only Lambda's s, which needs absolute accuracy ~1e-7: DESIGN.md
+// §4.1); D_P = C / (pi ax ay R N P) from the fp32 denominator (relative 3e-7).
+// Nothing when C = 0 or an fp64 cosine is not > 0 (DESIGN.md §4.3 S9).
+// Out of line: inlined, its code and registers cost the draw loop ~10 % even
+// though few lanes take it. Every scene value arrives as a scalar argument (a
+// pointer into the kernel's parameter space would force a local copy of the
+// whole scene per thread).
+__device__ __noinline__ float3 radiance_shell64(int ndf_kind, int view_kind, int light_kind, float vx, float vy, float vz,
+                                                float lx, float ly, float lz, float ir, float ig, float ib, float f0r,
+                                                float f0g, float f0b, float4 nrm, float4 pos, float ti, float bi,
+                                                float to, float bo, float ax2, float ay2, float den_f, float C) {
+  const float3 zero = make_float3(0.0f, 0.0f, 0.0f);
+  if (!(C > 0.0f)) return zero;
+  const double px = pos.x, py = pos.y, pz = pos.z;
+  const double nx = nrm.x, ny = nrm.y, nz = nrm.z;
+  double wx = vx, wy = vy, wz = vz;   // towards the viewer (pinhole camera or direction)
+  if (view_kind == 0) { wx -= px; wy -= py; wz -= pz; }
+  double ox = lx, oy = ly, oz = lz;   // towards the light
+  if (light_kind == 0) { ox -= px; oy -= py; oz -= pz; }
+  const double rn = rsqrt_d(dot3d(nx, ny, nz, nx, ny, nz));
+  const double ri = rsqrt_d(dot3d(wx, wy, wz, wx, wy, wz));
+  const double ro = rsqrt_d(dot3d(ox, oy, oz, ox, oy, oz));
+  const double ci = dot3d(nx, ny, nz, wx, wy, wz) * rn * ri;
+  const double co = dot3d(nx, ny, nz, ox, oy, oz) * rn * ro;
+  if (!(ci > 0.0) || !(co > 0.0)) return zero;
+  // Schlick F = f0 + (1 - f0)(1 - w_i.h)^5, h = normalize(w_i + w_o)
+  wx *= ri; wy *= ri; wz *= ri;
+  ox *= ro; oy *= ro; oz *= ro;
+  const double hx = wx + ox, hy = wy + oy, hz = wz + oz;
+  const double cih = dot3d(wx, wy, wz, hx, hy, hz) * rsqrt_d(dot3d(hx, hy, hz, hx, hy, hz));
   const double om = 1.0 - cih;
   const double om2 = om * om;
   const double om5 = om2 * om2 * om;
-  rgb.x += (float)(fma(1.0 - (double)sc.f0[0], om5, (double)sc.f0[0]) * (k * (double)lt.intensity[0]));
-  rgb.y += (float)(fma(1.0 - (double)sc.f0[1], om5, (double)sc.f0[1]) * (k * (double)lt.intensity[1]));
-  rgb.z += (float)(fma(1.0 - (double)sc.f0[2], om5, (double)sc.f0[2]) * (k * (double)lt.intensity[2]));
+  // G2 D_P E / (4 n.wi) = C E G2 / (4 n.wi pi ax ay R N P), one reciprocal
+  double ni_, di_, no_, do_;
+  lambda_frac(ndf_kind, (double)__fmaf_rn(ax2, ti * ti, ay2 * (bi * bi)), ci, ni_, di_);
+  lambda_frac(ndf_kind, (double)__fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co, no_, do_);
+  const double dd = di_ * do_;
+  const double E = light_kind == 0 ? ro * ro : 1.0;
+  const double k = ((double)C * E) * dd * rcp_d((fma(ni_, do_, dd) + no_ * di_) * (4.0 * ci) * (double)den_f);
+  const double f0d[3] = {f0r, f0g, f0b};
+  return make_float3((float)(fma(1.0 - f0d[0], om5, f0d[0]) * k * (double)ir),
+                     (float)(fma(1.0 - f0d[1], om5, f0d[1]) * k * (double)ig),
+                     (float)(fma(1.0 - f0d[2], om5, f0d[2]) * k * (double)ib));
+}
+
+// The fp32 tier. Its cosines come from the decision path (fp32-normalised
+// vectors, fp32 differences: absolute error <= ~5e-7, so relative <= 3.2e-5
+// at 2^-6); Lambda's tangential parts need only absolute accuracy (~2e-7,
+// the fp32 frame); Schlick's (1 - w_i.h)^5 with absolute error ~3e-7 adds
+// <= 5e-6 relative when f0 >= 2^-10.
+__device__ __forceinline__ float lambda32(int kind, float s, float c) {
+  if (!(s > 0.0f)) return 0.0f;
+  if (kind == 0) {
+    const float t = __fmaf_rn(c, c, s);
+    return __fdividef(s, 2.0f * c * (c + t * rsqrtf(t)));
+  }
+  const float a = c * rsqrtf(s);
+  if (a >= 1.6f) return 0.0f;
+  return __fdividef(__fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f), a * __fmaf_rn(2.181f, a, 3.535f));
+}
+// one light's contribution; ci, lam_i, dq: the pixel's cosine, Lambda(w_i)
+// and 4 n.wi pi ax ay R N P; rs = rsqrt_c(|d|^2). Only k = C G2 E / dq needs
+// a range check: F in [2^-10, 1], so F k stays normal, and the final product
+// with the intensity is one correctly rounded multiplication (an fp32 result
+// beyond fp32's range is that value's rounding)
+__device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, const glint_light& lt, float ci, float lam_i,
+                                                 float co, float cih, float to, float bo, float ax2, float ay2,
+                                                 float dq, float rs, float C, float3& rgb) {
+  if (!(ci >= 0x1p-6f && co >= 0x1p-6f)) return false;
+  const float om = 1.0f - cih;
+  const float om2 = om * om;
+  const float om5 = om2 * om2 * om;
+  const float g2 = __fdividef(1.0f, 1.0f + lam_i + lambda32(sc.ndf_kind, __fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co));
+  const float E = lt.kind == 0 ? rs * rs : 1.0f;
+  const float k = __fdividef(C * g2, dq) * E;
+  if (!(k >= 0x1p-100f && k <= 0x1p100f)) return false;
+  rgb.x += ((sc.f0[0] + (1.0f - sc.f0[0]) * om5) * k) * lt.intensity[0];
+  rgb.y += ((sc.f0[1] + (1.0f - sc.f0[1]) * om5) * k) * lt.intensity[1];
+  rgb.z += ((sc.f0[2] + (1.0f - sc.f0[2]) * om5) * k) * lt.intensity[2];
+  return true;
 }
 
 // shared tables at namespace scope: fixed shared-window offsets, so the
@@ -343,7 +377,8 @@ template <bool DEBUG, int MODE>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
-                                            uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n) {
+                                            uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n,
+                                            bool f0_fast) {
   const int L = sc.n_lights;
   uint32_t flags = 0;
   const uint32_t meta = __float_as_uint(uvm.w);
@@ -483,7 +518,12 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   view_dir(sc, pos, wix, wiy, wiz);
   const float ni = dot3(nx, ny, nz, wix, wiy, wiz);
   const float iax = rcp_c(ax), iay = rcp_c(ay);
+  // radiance accumulator, the fp32 tangential parts of w_i in the frame, and
+  // the pixel's shell constants (computed at its first glint, S9)
   float3 rgb = make_float3(0.0f, 0.0f, 0.0f);
+  bool have_px = false;
+  float ci_c = 0.0f, lam_i = 0.0f, dq = 0.0f;
+  const float ti = dot3(wix, wiy, wiz, tx, ty, tz), bi = dot3(wix, wiy, wiz, bx, by, bz);
 
   for (int l = 0; l < L; ++l) {
     const glint_light& lt = sc.lights[l];
@@ -691,7 +731,30 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     // ---------------- S8/S9: D_P and radiance (Eq. 1-3), fp64 shell.
     // Warp-uniform: lanes with C = 0 add exactly nothing (the shell returns
     // at once), so the block runs without per-lane divergence
-    if (DEBUG ? (C > 0.0f) : __any_sync(am, C > 0.0f)) radiance_shell(sc, lt, nrm, pos, ax, ay, R, N, P, C, rgb);
+    if (DEBUG ? (C > 0.0f) : __any_sync(am, C > 0.0f)) {
+      if (C > 0.0f) {
+        if (!have_px) {   // the pixel's shell constants, once (per-pixel work shared by the lights)
+          have_px = true;
+          ci_c = ni;
+          lam_i = lambda32(sc.ndf_kind, __fmaf_rn(ax * ax, ti * ti, ay * ay * (bi * bi)), ci_c);
+          dq = 3.14159265358979f * ax * ay * R * N * P * (4.0f * ci_c);
+        }
+        // w_o's tangential parts by reflecting w_i about h (fp32 frame): w_o = 2 (w_i.h) h - w_i
+        const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
+        const float to = __fmaf_rn(2.0f * cih, hx, -ti), bo = __fmaf_rn(2.0f * cih, hy, -bi);
+        const float rs = rsqrt_c(d2);   // the decision path's (dl = d2 rs)
+        if (!(f0_fast && radiance_shell32(sc, lt, ci_c, lam_i, nd * rs, cih, to, bo, ax * ax, ay * ay, dq, rs, C, rgb))) {
+          const float3 c = radiance_shell64(sc.ndf_kind, sc.view_kind, lt.kind, sc.view[0], sc.view[1], sc.view[2],
+                                            lt.pos_or_dir[0], lt.pos_or_dir[1], lt.pos_or_dir[2], lt.intensity[0],
+                                            lt.intensity[1], lt.intensity[2], sc.f0[0], sc.f0[1], sc.f0[2], nrm, pos,
+                                            ti, bi, to, bo, ax * ax, ay * ay, 3.14159265358979f * ax * ay * R * N * P,
+                                            C);
+          rgb.x += c.x;
+          rgb.y += c.y;
+          rgb.z += c.z;
+        }
+      }
+    }
   }
   if (DEBUG) for (int l = 0; l < L; ++l) rec[l].flags = flags;
   __stcs(outp, make_float4(rgb.x, rgb.y, rgb.z, __uint_as_float(flags)));
@@ -796,7 +859,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
                 oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
       shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
-                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n);
+                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0);
     }
     __syncwarp();
     if (lane == 0) {

@@ -50,6 +50,7 @@ struct KParams {
   uint32_t c1s, c1n;    // both 0x7feb352d (the draw hash's first multiplier), passed
                         // as two runtime values so that ptxas cannot prove them
                         // equal and re-factor hs*C1 + ka*C1 into (hs + ka)*C1 per draw
+  int32_t f0_fast;      // every f0 >= 2^-10: the fp32 tier of the S9 shell may be used
   glint_scene sc;
 };
 
