@@ -104,6 +104,39 @@ int main(void) {
   cudaFree(dout2);
   free(out_b);
 
+  /* the same frame as two row bands (a sharded frame): each band's
+     planes start at its first row, its tile origin (x0, y0) places it in one
+     full-frame output; the assembled frame equals the whole-frame launch */
+  void* dband;
+  if (cudaMalloc(&dband, 16 * n) != cudaSuccess) return 1;
+  const int H0 = 24;
+  glint_gbuffer bands[2] = {gb, gb};
+  bands[0].height = H0;
+  bands[1].height = H - H0;
+  bands[1].y0 = H0;
+  bands[1].duv = (const char*)gb.duv + 16 * (size_t)H0 * W;
+  bands[1].uvm = (const char*)gb.uvm + 16 * (size_t)H0 * W;
+  bands[1].nrm = (const char*)gb.nrm + 16 * (size_t)H0 * W;
+  bands[1].pos = (const char*)gb.pos + 16 * (size_t)H0 * W;
+  bands[1].mat = (const char*)gb.mat + 16 * (size_t)H0 * W;
+  glint_scene bsc[2] = {sc, sc};
+  void* bouts[2] = {dband, dband};
+  CHECK(glint_eval_batch(ctx, 2, bands, bsc, bouts, pitches, NULL));
+  float* out_bands = (float*)malloc(16 * n);
+  if (cudaMemcpy(out_bands, dband, 16 * n, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  int bands_same = memcmp(out, out_bands, 16 * n) == 0;
+  cudaFree(dband);
+  free(out_bands);
+
+  /* the metric's unit: active (pixel, light) pairs */
+  unsigned long long* dcount;
+  unsigned long long active = 0;
+  if (cudaMalloc((void**)&dcount, sizeof *dcount) != cudaSuccess) return 1;
+  cudaMemset(dcount, 0, sizeof *dcount);
+  CHECK(glint_count_active(ctx, &gb, &sc, dcount, NULL));
+  if (cudaMemcpy(&active, dcount, sizeof active, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+  cudaFree(dcount);
+
   int glints = 0;
   double sum = 0.0;
   for (size_t i = 0; i < n; ++i) {
@@ -112,12 +145,12 @@ int main(void) {
   }
   int same = memcmp(out, out_h, 16 * n) == 0;
   printf("glinting pixels %d of %zu, radiance sum %.9g, host entry identical %d, batch identical %d, "
-         "aliased batch refused %d, launches %lld\n", glints, n, sum, same, batch_same, alias_rc == GLINT_EALIAS,
-         (long long)glint_launch_count(ctx));
+         "aliased batch refused %d, bands identical %d, active pairs %llu, launches %lld\n", glints, n, sum, same,
+         batch_same, alias_rc == GLINT_EALIAS, bands_same, active, (long long)glint_launch_count(ctx));
   CHECK(glint_destroy(ctx));
   for (int p = 0; p < 5; ++p) { cudaFree(dev[p]); free(host[p]); }
   cudaFree(dout);
   free(out);
   free(out_h);
-  return (glints > 0 && same && batch_same && alias_rc == GLINT_EALIAS) ? 0 : 2;
+  return (glints > 0 && same && batch_same && alias_rc == GLINT_EALIAS && bands_same && active == n) ? 0 : 2;
 }

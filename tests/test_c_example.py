@@ -38,7 +38,7 @@ def test_c_example_runs_and_matches_python(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     m = re.search(r"glinting pixels (\d+) of 4096, radiance sum ([0-9.e+-]+), host entry identical 1, "
-                  r"batch identical 1, aliased batch refused 1", r.stdout)
+                  r"batch identical 1, aliased batch refused 1, bands identical 1, active pairs 4096", r.stdout)
     assert m, r.stdout
     fr = synth.c1("ggx", "mirror")
     ctx = pkg.Context(0)
