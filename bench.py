@@ -279,7 +279,13 @@ def run_ours(args):
     from paper_2306_05051_b200 import dist as D
     if int(os.environ.get("RANK", "0")) == 0:
         B.build()
-    rank, world, local = D.init("nccl")
+    # GLINT_BENCH_BACKEND=gloo and GLINT_BENCH_DEVICE=<d> exist for the
+    # functional test of the N > 1 code path on one GPU
+    # (tests/test_bench_contract.py::test_our_arm_two_ranks_one_gpu); a
+    # measurement always runs NCCL with one GPU per rank
+    backend = os.environ.get("GLINT_BENCH_BACKEND", "nccl")
+    rank, world, local = D.init(backend)
+    local = int(os.environ.get("GLINT_BENCH_DEVICE", local))
     if world > 1:
         D.barrier()
     torch.cuda.set_device(local)
@@ -310,6 +316,8 @@ def run_ours(args):
 
     # ---- outputs: rank 0 owns the step's full frames; the gather is in the timed region
     use_nccl = world > 1 and args.gather == "nccl"
+    if use_nccl and backend != "nccl":
+        raise SystemExit("--gather nccl needs the NCCL backend")
     comm = torch.cuda.Stream(dev) if use_nccl else None
     if use_nccl:
         full = torch.empty((n_frames, H, W, 4), dtype=torch.float32, device=dev) if rank == 0 else None

@@ -14,7 +14,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    # fp contract of DESIGN.md §4: no FMA contraction, IEEE div/sqrt, no FTZ
+    # fp contract of DESIGN.md §4: no FMA contraction, no FTZ; -prec-div keeps the one
+    # IEEE division per scene (1 / beta) exact (the decision path divides only through rcp_c)
     "-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false",
     "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
 ]

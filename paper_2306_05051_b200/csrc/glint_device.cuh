@@ -4,7 +4,9 @@
 // DESIGN.md §4 (bit-exact with the CPU oracle on every value that decides an
 // integer). The translation unit is compiled with -fmad=false so that a*b+c
 // stays two roundings; FMAs appear only as explicit __fmaf_rn where the
-// contract writes fma. No fast-math, no FTZ, IEEE div/sqrt.
+// contract writes fma. No fast-math, no FTZ; division and square root on the
+// decision path only through the contract's rcp_c / rsqrt_c (Newton steps from a
+// magic-constant seed, no MUFU), plus one IEEE division per scene (1 / beta).
 //
 // P:Lnnn = line of the paper's text (arXiv 2306.05051).
 #pragma once

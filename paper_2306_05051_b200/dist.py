@@ -73,10 +73,15 @@ def plan_tiles(n_frames: int, height: int, world: int, band_rows: int = 64) -> L
     return [(f, y0, y1) for f in range(n_frames) for (y0, y1) in row_bands(height, band_rows)]
 
 
+def _reduce_device(device):
+    """gloo reduces host tensors; NCCL device tensors."""
+    return "cpu" if dist.get_backend() == "gloo" else device
+
+
 def max_over_ranks(x: float, device=None) -> float:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -84,7 +89,7 @@ def max_over_ranks(x: float, device=None) -> float:
 def sum_over_ranks(x: float, device=None) -> float:
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 

@@ -81,3 +81,40 @@ def test_our_arm_json_line_on_the_gpu():
         assert c["sm_mhz"] > 0 and c["sm_max_mhz"] > 0
     else:
         assert c["reasons"] == ["nvml_unavailable"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["C3", "C2"])
+def test_our_arm_two_ranks_one_gpu(config):
+    """The N > 1 code path of our arm, functionally, on the one GPU of this
+    box: torchrun with 2 ranks, both on cuda:0 (GLINT_BENCH_DEVICE), gloo for
+    the control plane (NCCL refuses two ranks on one device). C3 is one frame
+    cut into 64-row bands, C2 ten whole frames dealt to 2 ranks; rank 1's
+    kernels store its tiles through their tile origins into rank 0's
+    IPC-mapped full frames (the fused gather). Rank 0 alone prints one line
+    with n_gpus 2; every pixel was written and rank-1 tiles re-evaluated on
+    rank 0 are bit-identical. (Timing here is meaningless: two processes share
+    one GPU.)"""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
+           "--config", config, "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+    env = dict(os.environ, GLINT_BENCH_BACKEND="gloo", GLINT_BENCH_DEVICE="0")
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    cf = d["config"]
+    assert "bit-identical" in cf["verified"] and "fused" in cf["gather"]
+    assert ("64-row bands" in cf["parallelism"]) == (config == "C3")
+    assert d["gpu_launches"] == 2 * cf["tiles_per_step"]
+
+
+def test_bench_refuses_a_mismatched_world():
+    """--gpus N under a world of another size prints no result line."""
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--impl", "reference", "--steps", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and not any(ln.startswith("{") for ln in r.stdout.splitlines())
+    assert "refusing" in r.stderr

@@ -193,7 +193,7 @@ def test_full_size_c2_sampled(ctx):
 @pytest.mark.timeout(300)
 def test_full_size_c4_sampled(ctx):
     """A full 3840x2160 C4 frame (32 spheres, 16 lights) in the bench's launch
-    configuration (production kernel: sparse gates and warp votes over lanes
+    configuration (production kernel: warp-vote grid skips and the warp-uniform radiance block over lanes
     with mixed light visibility); sampled pixels recomputed by the oracle."""
     import oracle
     import paper_2306_05051_b200 as pkg
