@@ -24,7 +24,7 @@ __device__ __forceinline__ float pow2half(int e) {
 
 // exp2c(y), y <= 0 (Eq. 16 (1-p)^n and the Beckmann exponential). DESIGN §4.2.
 __device__ __forceinline__ float exp2c(float y) {
-  const bool under = !(y >= -125.0f);   // -> 0 (select, branch-free)
+  const bool under = !(y >= -125.0f);   // -> 0 (branch-free: the polynomial always runs)
   y = under ? 0.0f : y;
   // k = rint(y) by the 1.5 2^23 magic number; 2^k from K's bits
   const float K = y + 12582912.0f;
@@ -39,7 +39,7 @@ __device__ __forceinline__ float exp2c(float y) {
   q = __fmaf_rn(q, f, 0x1.62e430p-1f);
   q = __fmaf_rn(q, f, 1.0f);
   const float p2 = __uint_as_float((__float_as_uint(K) - 0x4B3FFF81u) << 23);   // 2^k
-  return under ? 0.0f : q * p2;
+  return (q * p2) * (under ? 0.0f : 1.0f);   // a select as a multiply keeps ptxas from branching
 }
 
 // 1/x for normal x > 0: magic start + 3 Newton steps, branch-free;
@@ -142,19 +142,21 @@ struct Gate {
   float sigma, m1, cap;
 };
 __device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
-  // L2 = log2(1 - p) for p in (0,1), precomputed once per (pixel, light)
+  // L2 = log2(1 - p) for p in (0,1) and -inf for p = 1 (then exp2c(n L2) = 0
+  // and P>=1 = 1 with no select), precomputed once per (pixel, light);
   // branch-free. For n <= 0 or p <= 0 only T needs forcing (to 0): the
   // sigma / m1 / cap of such a grid are never used (its count is 0), and
   // the DEBUG record reports the contract's values (0, 1, 1) explicitly.
   Gate g;
   const bool none = !(n > 0.0f) || !(p > 0.0f);
-  const float pge1 = (p >= 1.0f) ? 1.0f : 1.0f - exp2c(n * L2);
+  const float pge1 = 1.0f - exp2c(n * L2);
   const uint32_t T = __float2uint_ru(pge1 * 0x1p23f);   // = (uint32_t)ceil(P>=1 2^23), exact
   const float nm1 = n - 1.0f;
   const float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
   const float var = mu * (1.0f - p);
   g.T = none ? 0u : T;
-  g.sigma = var >= 0x1p-126f ? var * rsqrt_c(var) : 0.0f;   // contract sqrt (subnormal -> 0)
+  const float rv = rsqrt_c(fmaxf(var, 0x1p-126f));          // always computed: no branch
+  g.sigma = var >= 0x1p-126f ? var * rv : 0.0f;              // contract sqrt (subnormal -> 0)
   g.m1 = 1.0f + mu;
   g.cap = ceilf(n);
   return g;

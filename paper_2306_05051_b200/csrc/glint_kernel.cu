@@ -581,7 +581,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
-    const float L2 = (p > 0.0f && p < 1.0f) ? log2_1mp(p) : 0.0f;
+    const float L2 = p >= 1.0f ? -__int_as_float(0x7f800000) : (p > 0.0f ? log2_1mp(p) : 0.0f);   // see gate_params
     float A[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // A_j = sum_ik beta_ik c_ikj
     if (MODE == 3) {
       // ---- Zirr & Kaplanyan-style baseline: per LOD of
