@@ -347,21 +347,23 @@ __device__ __forceinline__ float lambda32(int kind, float s, float c) {
 // a range check: F in [2^-10, 1], so F k stays normal, and the final product
 // with the intensity is one correctly rounded multiplication (an fp32 result
 // beyond fp32's range is that value's rounding)
-__device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, const glint_light& lt, float ci, float lam_i,
+__device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, int ndf, const glint_light& lt, float ci, float lam_i,
                                                  float co, float cih, float to, float bo, float ax2, float ay2,
                                                  float dq, float rs, float C, float3& rgb) {
-  if (!(ci >= 0x1p-6f && co >= 0x1p-6f)) return false;
   const float om = 1.0f - cih;
   const float om2 = om * om;
   const float om5 = om2 * om2 * om;
-  const float g2 = __fdividef(1.0f, 1.0f + lam_i + lambda32(sc.ndf_kind, __fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co));
+  const float g2 = __fdividef(1.0f, 1.0f + lam_i + lambda32(ndf, __fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co));
   const float E = lt.kind == 0 ? rs * rs : 1.0f;
   const float k = __fdividef(C * g2, dq) * E;
-  if (!(k >= 0x1p-100f && k <= 0x1p100f)) return false;
-  rgb.x += ((sc.f0[0] + (1.0f - sc.f0[0]) * om5) * k) * lt.intensity[0];
-  rgb.y += ((sc.f0[1] + (1.0f - sc.f0[1]) * om5) * k) * lt.intensity[1];
-  rgb.z += ((sc.f0[2] + (1.0f - sc.f0[2]) * om5) * k) * lt.intensity[2];
-  return true;
+  // one exit (no branches): a lane outside the tier adds an exact +0 and
+  // returns false, so the caller's fp64 tier adds its contribution instead
+  const bool ok = ci >= 0x1p-6f && co >= 0x1p-6f && k >= 0x1p-100f && k <= 0x1p100f;
+  const float kk = ok ? k : 0.0f;
+  rgb.x += ((sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk) * lt.intensity[0];
+  rgb.y += ((sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk) * lt.intensity[1];
+  rgb.z += ((sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk) * lt.intensity[2];
+  return ok;
 }
 
 // shared tables at namespace scope: fixed shared-window offsets, so the
@@ -373,12 +375,16 @@ __shared__ __align__(16) float2 g_sCS[GLINT_NANG];
 // Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
 // pixel's output float4, `rec` its first debug record (DEBUG only).
 // ---------------------------------------------------------------------------
-template <bool DEBUG, int MODE>
+// NDF: the scene's ndf_kind fixed at compile time (0 GGX, 1 Beckmann) for the
+// production kernel of the method, -1 = read from the scene (DEBUG, ablations,
+// baseline): the GGX / Beckmann branches of S5 and of the shell disappear
+template <bool DEBUG, int MODE, int NDF>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
                                             uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n,
                                             bool f0_fast) {
+  const int ndf = NDF >= 0 ? NDF : sc.ndf_kind;
   const int L = sc.n_lights;
   uint32_t flags = 0;
   const uint32_t meta = __float_as_uint(uvm.w);
@@ -554,7 +560,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       const float X = hx * iax, Y = hy * iay;
       const float s2 = X * X + Y * Y;
       const float hz2 = hz * hz;
-      if (sc.ndf_kind == 0) {
+      if (ndf == 0) {
         const float q = s2 + hz2;
         ratio = rcp_c(q * q);
       } else {
@@ -736,15 +742,15 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         if (!have_px) {   // the pixel's shell constants, once (per-pixel work shared by the lights)
           have_px = true;
           ci_c = ni;
-          lam_i = lambda32(sc.ndf_kind, __fmaf_rn(ax * ax, ti * ti, ay * ay * (bi * bi)), ci_c);
+          lam_i = lambda32(ndf, __fmaf_rn(ax * ax, ti * ti, ay * ay * (bi * bi)), ci_c);
           dq = 3.14159265358979f * ax * ay * R * N * P * (4.0f * ci_c);
         }
         // w_o's tangential parts by reflecting w_i about h (fp32 frame): w_o = 2 (w_i.h) h - w_i
         const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
         const float to = __fmaf_rn(2.0f * cih, hx, -ti), bo = __fmaf_rn(2.0f * cih, hy, -bi);
         const float rs = rsqrt_c(d2);   // the decision path's (dl = d2 rs)
-        if (!(f0_fast && radiance_shell32(sc, lt, ci_c, lam_i, nd * rs, cih, to, bo, ax * ax, ay * ay, dq, rs, C, rgb))) {
-          const float3 c = radiance_shell64(sc.ndf_kind, sc.view_kind, lt.kind, sc.view[0], sc.view[1], sc.view[2],
+        if (!(f0_fast && radiance_shell32(sc, ndf, lt, ci_c, lam_i, nd * rs, cih, to, bo, ax * ax, ay * ay, dq, rs, C, rgb))) {
+          const float3 c = radiance_shell64(ndf, sc.view_kind, lt.kind, sc.view[0], sc.view[1], sc.view[2],
                                             lt.pos_or_dir[0], lt.pos_or_dir[1], lt.pos_or_dir[2], lt.intensity[0],
                                             lt.intensity[1], lt.intensity[2], sc.f0[0], sc.f0[1], sc.f0[2], nrm, pos,
                                             ti, bi, to, bo, ax * ax, ay * ay, 3.14159265358979f * ax * ay * R * N * P,
@@ -772,7 +778,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 // barrier inside the loop; a warp can run up to kStages - 1 tiles ahead of
 // the slowest one. Without TMA the ring carries only tile ids.
 // ---------------------------------------------------------------------------
-template <bool DEBUG, bool TMA, int MODE>
+template <bool DEBUG, bool TMA, int MODE, int NDF>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
   float* sZ = g_sZ;
   float2* sCS = g_sCS;
@@ -858,7 +864,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       }
       GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
                 oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
-      shade_pixel<DEBUG, MODE>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
+      shade_pixel<DEBUG, MODE, NDF>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
                                nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0);
     }
     __syncwarp();
@@ -888,7 +894,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   }
 }
 
-template <bool DEBUG, bool TMA, int MODE>
+template <bool DEBUG, bool TMA, int MODE, int NDF = -1>
 static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, bool pdl) {
   const size_t smem = TMA ? kSmemTma : kSmemTables;
   // the dynamic shared-memory opt-in, once per (instantiation, device);
@@ -900,13 +906,13 @@ static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, b
   if (e != cudaSuccess) return e;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE, NDF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
   if (!pdl) {
-    glint_eval_kernel<DEBUG, TMA, MODE><<<grid, kBlock, smem, stream>>>(prm);
+    glint_eval_kernel<DEBUG, TMA, MODE, NDF><<<grid, kBlock, smem, stream>>>(prm);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -919,7 +925,7 @@ static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, b
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, glint_eval_kernel<DEBUG, TMA, MODE>, prm);
+  return cudaLaunchKernelEx(&cfg, glint_eval_kernel<DEBUG, TMA, MODE, NDF>, prm);
 }
 
 cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream, bool pdl) {
@@ -935,7 +941,9 @@ cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t s
     case 3:
       return tma ? launch_t<false, true, 3>(prm, grid, stream, pdl) : launch_t<false, false, 3>(prm, grid, stream, pdl);
     default:
-      return tma ? launch_t<false, true, 0>(prm, grid, stream, pdl) : launch_t<false, false, 0>(prm, grid, stream, pdl);
+      if (prm.sc.ndf_kind == 0)
+        return tma ? launch_t<false, true, 0, 0>(prm, grid, stream, pdl) : launch_t<false, false, 0, 0>(prm, grid, stream, pdl);
+      return tma ? launch_t<false, true, 0, 1>(prm, grid, stream, pdl) : launch_t<false, false, 0, 1>(prm, grid, stream, pdl);
   }
 }
 
@@ -980,10 +988,10 @@ cudaError_t launch_count_active(const float4* duv, const float4* uvm, const floa
 }
 
 cudaError_t occupancy_blocks_per_sm(int* out) {
-  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemTma);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true, 0>, kBlock, kSmemTma);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true, 0, 0>, kBlock, kSmemTma);
 }
 
 }  // namespace glint

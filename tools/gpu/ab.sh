@@ -6,8 +6,8 @@
 cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 for l in paper_2306_05051_b200/libglint.so $1; do
-  for cfg in C2 C5; do
-    st=30; [ $cfg = C5 ] && st=5
+  for cfg in ${AB_CONFIGS:-C2 C5}; do
+    st=30; [ $cfg = C5 ] && st=5; [ $cfg = C4 ] && st=10
     n=$(basename $l .so)_$cfg
     GLINT_LIB=$PWD/$l timeout 600 python bench.py --config $cfg --steps $st --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ab_$n.json 2> gpurun_out/ab_$n.err
     v=$(tail -1 gpurun_out/ab_$n.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.4e %.3f ms %s' % (d['value'], d['ms_per_step'], d['clocks']['sm_mhz']))" 2>/dev/null)
