@@ -332,15 +332,31 @@ __device__ __noinline__ float3 radiance_shell64(int ndf_kind, int view_kind, int
 // at 2^-6); Lambda's tangential parts need only absolute accuracy (~2e-7,
 // the fp32 frame); Schlick's (1 - w_i.h)^5 with absolute error ~3e-7 adds
 // <= 5e-6 relative when f0 >= 2^-10.
+// MUFU reciprocal / rsqrt with flush-to-zero (one instruction each; without
+// .ftz the compiler wraps every MUFU op in ~4 instructions of subnormal
+// scaling). Every value the fp32 tier accepts is a normal float: its
+// cosines are >= 2^-6 and k is range-checked; a flushed operand can only
+// yield 0 / inf / NaN in k (rejected: the lane takes the fp64 tier) or a
+// Beckmann a = inf (Lambda = 0, the s -> 0 limit).
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float lambda32(int kind, float s, float c) {
   if (!(s > 0.0f)) return 0.0f;
   if (kind == 0) {
     const float t = __fmaf_rn(c, c, s);
-    return __fdividef(s, 2.0f * c * (c + t * rsqrtf(t)));
+    return s * rcp_ftz(2.0f * c * (c + t * rsqrt_ftz(t)));
   }
-  const float a = c * rsqrtf(s);
+  const float a = c * rsqrt_ftz(s);
   if (a >= 1.6f) return 0.0f;
-  return __fdividef(__fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f), a * __fmaf_rn(2.181f, a, 3.535f));
+  return __fmaf_rn(a, __fmaf_rn(0.396f, a, -1.259f), 1.0f) * rcp_ftz(a * __fmaf_rn(2.181f, a, 3.535f));
 }
 // one light's contribution; ci, lam_i, dq: the pixel's cosine, Lambda(w_i)
 // and 4 n.wi pi ax ay R N P; rs = rsqrt_c(|d|^2). Only k = C G2 E / dq needs
@@ -353,9 +369,9 @@ __device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, int ndf,
   const float om = 1.0f - cih;
   const float om2 = om * om;
   const float om5 = om2 * om2 * om;
-  const float g2 = __fdividef(1.0f, 1.0f + lam_i + lambda32(ndf, __fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co));
+  const float g2 = rcp_ftz(1.0f + lam_i + lambda32(ndf, __fmaf_rn(ax2, to * to, ay2 * (bo * bo)), co));
   const float E = lt.kind == 0 ? rs * rs : 1.0f;
-  const float k = __fdividef(C * g2, dq) * E;
+  const float k = (C * g2) * rcp_ftz(dq) * E;
   // one exit (no branches): a lane outside the tier adds an exact +0 and
   // returns false, so the caller's fp64 tier adds its contribution instead
   const bool ok = ci >= 0x1p-6f && co >= 0x1p-6f && k >= 0x1p-100f && k <= 0x1p100f;
