@@ -400,6 +400,7 @@ def run_ours(args):
     if clk.rejected():
         ms, launches, clk = timed()
     ms_max = D.max_over_ranks(ms, device=dev)
+    ms_rank0 = ms            # printed by rank 0: its own timed region (with NCCL, its last receive)
     evals_all = D.sum_over_ranks(evals, device=dev) * args.steps
     evals_repl_all = D.sum_over_ranks(evals_replicated, device=dev) * args.steps
     launches_all = int(round(D.sum_over_ranks(float(launches), device=dev)))
@@ -429,6 +430,26 @@ def run_ours(args):
         check = (f"all {n_frames} frames written at rank 0; {len(remote)} tiles from other ranks "
                  f"re-evaluated on rank 0: bit-identical") if remote else f"all {n_frames} frames written"
     D.barrier()
+
+    # ---- compute-only scaling (N > 1): the same steps with each rank's tiles
+    # shaded into local buffers, no gather; max over ranks of the device time
+    compute_only = None
+    if world > 1:
+        louts = [torch.empty((tiles[i][2] - tiles[i][1], W, 4), dtype=torch.float32, device=dev) for i in mine]
+        for _ in range(2):
+            pkg.glint_eval_batch(ctx, gbs, scenes, outs=louts, stream=stream)
+        torch.cuda.synchronize()
+        D.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            pkg.glint_eval_batch(ctx, gbs, scenes, outs=louts, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        c_ms = D.max_over_ranks(a.elapsed_time(b), device=dev)
+        compute_only = {"value": evals_all / (c_ms / 1e3), "ms_per_step": c_ms / args.steps,
+                        "how": "each rank's tiles into local buffers, no gather; max over ranks"}
+        del louts
 
     # ---- roofline of the dominant (only) kernel: issue-bound ALU path
     peaks, peak_src = load_peaks()
@@ -557,7 +578,8 @@ def run_ours(args):
                                   "memory over NVLink), inside the timed region" if not use_nccl else
                                   "NCCL grouped send/recv per tile round on a comm stream, each send after its "
                                   "tile's kernel event, inside the timed region"),
-                       "verified": check},
+                       "verified": check, "rank0_ms_per_step": ms_rank0 / args.steps,
+                       **({"compute_only": compute_only} if compute_only else {})},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_all,
             "clocks": cs, "gpu": props.name,
         }

@@ -109,6 +109,7 @@ def test_our_arm_two_ranks_one_gpu(config):
     assert "bit-identical" in cf["verified"] and "fused" in cf["gather"]
     assert ("64-row bands" in cf["parallelism"]) == (config == "C3")
     assert d["gpu_launches"] == 2 * cf["tiles_per_step"]
+    assert cf["compute_only"]["value"] > 0 and cf["rank0_ms_per_step"] > 0
 
 
 def test_bench_refuses_a_mismatched_world():

@@ -83,13 +83,13 @@ def _shade_tile_oracle(f, y0, y1, W=64, H=48):
     return torch.from_numpy(img)
 
 
-def _tile_worker(rank, world, port, n_frames, q):
+def _tile_worker(rank, world, port, n_frames, q, band_rows=16):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world),
                       LOCAL_RANK=str(rank))
     try:
         r, w, _ = D.init("gloo")
         H, W = 48, 64
-        tiles = D.plan_tiles(n_frames, H, w, band_rows=16)
+        tiles = D.plan_tiles(n_frames, H, w, band_rows=band_rows)
         g = D.TileGather(tiles, r, w, full=[torch.full((H, W, 4), float("nan")) for _ in range(n_frames)]
                          if r == 0 else None)
         local = {}
@@ -109,11 +109,11 @@ def _tile_worker(rank, world, port, n_frames, q):
         q.put((rank, repr(e), None))
 
 
-@pytest.mark.parametrize("n_frames", [1, 3])
-def test_gloo_tile_gather_assembles_the_single_rank_image(n_frames):
-    """SURVEY 8e at world size 2 on CPU: one frame cut into 16-row bands (C2 /
-    C3-style row-band sharding, the last band on the second rank) or three
-    whole frames (C4 / C5-style frame sharding), each tile shaded by its rank
+@pytest.mark.parametrize("world,n_frames", [(2, 1), (2, 3), (4, 1), (4, 3)])
+def test_gloo_tile_gather_assembles_the_single_rank_image(world, n_frames):
+    """SURVEY 8e at world sizes 2 and 4 on CPU: one frame cut into bands (C2 /
+    C3-style row-band sharding) or three frames (whole frames at 2 ranks,
+    bands of every frame at 4: fewer frames than ranks), each tile shaded by its rank
     (the oracle stands in for the kernel) and gathered to rank 0 by the
     per-tile send/recv rounds of dist.TileGather: rank 0's assembled frames
     equal the whole frames shaded in one process, bit for bit."""
@@ -121,7 +121,8 @@ def test_gloo_tile_gather_assembles_the_single_rank_image(n_frames):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_tile_worker, args=(r, 2, port, n_frames, q)) for r in range(2)]
+    band = 8 if world == 4 else 16
+    ps = [ctx.Process(target=_tile_worker, args=(r, world, port, n_frames, q, band)) for r in range(world)]
     for p in ps:
         p.start()
     res = {r: (full, tiles) for r, full, tiles in (q.get(timeout=300) for _ in ps)}
@@ -130,8 +131,11 @@ def test_gloo_tile_gather_assembles_the_single_rank_image(n_frames):
         assert p.exitcode == 0
     full, tiles = res[0]
     assert not isinstance(full, str), full
-    assert len(tiles) == (3 if n_frames == 1 else 3)            # 48 rows / 16 = 3 bands, or 3 frames
-    assert {i % 2 for i in range(len(tiles))} == {0, 1}         # both ranks shaded something
+    if n_frames == 1:
+        assert len(tiles) == 48 // band                          # the frame's bands
+    else:
+        assert len(tiles) == (3 if world <= 3 else 3 * (48 // band))   # whole frames, or bands of every frame
+    assert {i % world for i in range(len(tiles))} == set(range(world))   # every rank shaded something
     for f in range(n_frames):
         ref = _shade_tile_oracle(f, 0, 48).numpy()
         assert np.array_equal(full[f].view(np.uint32), ref.view(np.uint32)), f
