@@ -279,7 +279,6 @@ static void make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint
   k.c1n = 0x7feb352du;
   k.sc = *sc;
   k.f0_fast = sc->f0[0] >= 0x1p-10f && sc->f0[1] >= 0x1p-10f && sc->f0[2] >= 0x1p-10f;
-  for (int i = 0; i < 3; ++i) k.omf0[i] = 1.0f - sc->f0[i];
 }
 
 static int grid_for(const glint_ctx* c, int64_t n_pix) {

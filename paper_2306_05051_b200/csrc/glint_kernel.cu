@@ -363,8 +363,7 @@ __device__ __forceinline__ float lambda32(int kind, float s, float c) {
 // a range check: F in [2^-10, 1], so F k stays normal, and the final product
 // with the intensity is one correctly rounded multiplication (an fp32 result
 // beyond fp32's range is that value's rounding)
-__device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, float3 omf0, int ndf, const glint_light& lt,
-                                                 float ci, float lam_i,
+__device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, int ndf, const glint_light& lt, float ci, float lam_i,
                                                  float co, float cih, float to, float bo, float ax2, float ay2,
                                                  float dq, float rs, float C, float3& rgb) {
   const float om = 1.0f - cih;
@@ -377,9 +376,9 @@ __device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, float3 o
   // returns false, so the caller's fp64 tier adds its contribution instead
   const bool ok = ci >= 0x1p-6f && co >= 0x1p-6f && k >= 0x1p-100f && k <= 0x1p100f;
   const float kk = ok ? k : 0.0f;
-  rgb.x = __fmaf_rn(__fmaf_rn(omf0.x, om5, sc.f0[0]) * kk, lt.intensity[0], rgb.x);
-  rgb.y = __fmaf_rn(__fmaf_rn(omf0.y, om5, sc.f0[1]) * kk, lt.intensity[1], rgb.y);
-  rgb.z = __fmaf_rn(__fmaf_rn(omf0.z, om5, sc.f0[2]) * kk, lt.intensity[2], rgb.z);
+  rgb.x += ((sc.f0[0] + (1.0f - sc.f0[0]) * om5) * kk) * lt.intensity[0];
+  rgb.y += ((sc.f0[1] + (1.0f - sc.f0[1]) * om5) * kk) * lt.intensity[1];
+  rgb.z += ((sc.f0[2] + (1.0f - sc.f0[2]) * om5) * kk) * lt.intensity[2];
   return ok;
 }
 
@@ -400,7 +399,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
                                             uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n,
-                                            bool f0_fast, float3 omf0) {
+                                            bool f0_fast) {
   const int ndf = NDF >= 0 ? NDF : sc.ndf_kind;
   const int L = sc.n_lights;
   uint32_t flags = 0;
@@ -766,7 +765,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         const float cih = dot3(wix, wiy, wiz, hx_, hy_, hz_);
         const float to = __fmaf_rn(2.0f * cih, hx, -ti), bo = __fmaf_rn(2.0f * cih, hy, -bi);
         const float rs = rsqrt_c(d2);   // the decision path's (dl = d2 rs)
-        if (!(f0_fast && radiance_shell32(sc, omf0, ndf, lt, ci_c, lam_i, nd * rs, cih, to, bo, ax * ax, ay * ay, dq, rs, C, rgb))) {
+        if (!(f0_fast && radiance_shell32(sc, ndf, lt, ci_c, lam_i, nd * rs, cih, to, bo, ax * ax, ay * ay, dq, rs, C, rgb))) {
           const float3 c = radiance_shell64(ndf, sc.view_kind, lt.kind, sc.view[0], sc.view[1], sc.view[2],
                                             lt.pos_or_dir[0], lt.pos_or_dir[1], lt.pos_or_dir[2], lt.intensity[0],
                                             lt.intensity[1], lt.intensity[2], sc.f0[0], sc.f0[1], sc.f0[2], nrm, pos,
@@ -882,8 +881,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
                 oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
       shade_pixel<DEBUG, MODE, NDF>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
-                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0,
-                                  make_float3(prm.omf0[0], prm.omf0[1], prm.omf0[2]));
+                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0);
     }
     __syncwarp();
     if (lane == 0) {

@@ -51,7 +51,6 @@ struct KParams {
                         // as two runtime values so that ptxas cannot prove them
                         // equal and re-factor hs*C1 + ka*C1 into (hs + ka)*C1 per draw
   int32_t f0_fast;      // every f0 >= 2^-10: the fp32 tier of the S9 shell may be used
-  float omf0[3];        // 1 - f0 (fp32, Schlick's weight)
   glint_scene sc;
 };
 
