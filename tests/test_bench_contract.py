@@ -95,10 +95,15 @@ def test_our_arm_two_ranks_one_gpu(config):
     with n_gpus 2; every pixel was written and rank-1 tiles re-evaluated on
     rank 0 are bit-identical. (Timing here is meaningless: two processes share
     one GPU.)"""
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", "2",
-           "--config", config, "--steps", "2", "--warmup", "3", "--no-e2e", "--no-cpu-baseline"]
+    args = ["bench.py", "--gpus", "2", "--config", config, "--steps", "2", "--warmup", "3", "--no-e2e",
+            "--no-cpu-baseline"]
+    if config == "C3":    # launched as the driver does
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+               "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), *args]
+    else:                 # bench.py re-executes itself through torchrun (no WORLD_SIZE in the environment)
+        cmd = [sys.executable, *args]
     env = dict(os.environ, GLINT_BENCH_BACKEND="gloo", GLINT_BENCH_DEVICE="0")
+    env.pop("WORLD_SIZE", None)
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
