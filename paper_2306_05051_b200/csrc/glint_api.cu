@@ -242,20 +242,27 @@ static void* tile_out(void* out, const glint_gbuffer* g, int64_t out_pitch) {
 // slot of a ring (reused kSchedSlots launches later); a launch recorded by
 // stream capture owns a slot of a separate pool for good (its graph may be
 // replayed at any time alongside ordinary launches).
-static int sched_slots(const glint_ctx* c, cudaStream_t stream, int n, std::vector<unsigned long long*>& slots) {
+struct Slots {
+  int64_t first;   // first slot index of this call's run
+  bool ring;       // ordinary launches (ring) or graph-captured ones (pool)
+};
+static int sched_slots(const glint_ctx* c, cudaStream_t stream, int n, Slots* out) {
   glint_ctx* cm = const_cast<glint_ctx*>(c);
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   GL_CUDA(cudaStreamIsCapturing(stream, &st));
-  slots.resize(n);
-  if (st == cudaStreamCaptureStatusActive) {
-    const int64_t k = cm->capture_next.fetch_add(n);
-    if (k + n > glint::kCaptureSlots) return GLINT_ELIMIT;
-    for (int i = 0; i < n; ++i) slots[i] = c->d_sched + 2 * (glint::kSchedSlots + k + i);
+  out->ring = st != cudaStreamCaptureStatusActive;
+  if (out->ring) {
+    out->first = cm->sched_next.fetch_add(n);
   } else {
-    const int64_t k = cm->sched_next.fetch_add(n);
-    for (int i = 0; i < n; ++i) slots[i] = c->d_sched + 2 * ((k + i) % glint::kSchedSlots);
+    out->first = cm->capture_next.fetch_add(n);
+    if (out->first + n > glint::kCaptureSlots) return GLINT_ELIMIT;
   }
   return GLINT_OK;
+}
+// the counter pair of the i-th launch of a run
+static unsigned long long* slot_at(const glint_ctx* c, const Slots& s, int i) {
+  return s.ring ? c->d_sched + 2 * ((s.first + i) % glint::kSchedSlots)
+                : c->d_sched + 2 * (glint::kSchedSlots + s.first + i);
 }
 
 static void make_params(const glint_ctx* c, const glint_gbuffer* gb, const glint_scene* sc, void* out,
@@ -304,15 +311,11 @@ extern "C" int glint_eval(const glint_ctx* c, const glint_gbuffer* gb, const gli
   int cur = -1;
   GL_CUDA(cudaGetDevice(&cur));
   if (cur != c->device) return GLINT_EDEVICE;
-  std::vector<unsigned long long*> slot;
-  try {
-    rc = sched_slots(c, (cudaStream_t)stream, 1, slot);
-  } catch (...) {
-    return GLINT_ENOMEM;
-  }
+  Slots slot;
+  rc = sched_slots(c, (cudaStream_t)stream, 1, &slot);
   if (rc) return rc;
   glint::KParams k;
-  make_params(c, gb, sc, out, out_pitch, dbg, slot[0], &k);
+  make_params(c, gb, sc, out, out_pitch, dbg, slot_at(c, slot, 0), &k);
   int64_t n_pix = (int64_t)gb->width * gb->height;
   GL_CUDA(glint::launch_eval(k, grid_for(c, n_pix), dbg != nullptr, (cudaStream_t)stream));
   const_cast<glint_ctx*>(c)->launches++;
@@ -401,19 +404,15 @@ extern "C" int glint_eval_batch(const glint_ctx* c, int n_frames, const glint_gb
   if (cur != c->device) return GLINT_EDEVICE;
   int n_launch = 0;
   for (int f = 0; f < n_frames; ++f) n_launch += (gbs[f].width > 0 && gbs[f].height > 0) ? 1 : 0;
-  std::vector<unsigned long long*> slots;
-  try {
-    rc = sched_slots(c, (cudaStream_t)stream, n_launch, slots);
-  } catch (...) {
-    return GLINT_ENOMEM;
-  }
+  Slots slots;
+  rc = sched_slots(c, (cudaStream_t)stream, n_launch, &slots);
   if (rc) return rc;
   int i = 0;
   for (int f = 0; f < n_frames; ++f) {
     const glint_gbuffer& g = gbs[f];
     if (g.width == 0 || g.height == 0) continue;
     glint::KParams k;
-    make_params(c, &g, &scenes[f], outs[f], out_pitches[f], nullptr, slots[i], &k);
+    make_params(c, &g, &scenes[f], outs[f], out_pitches[f], nullptr, slot_at(c, slots, i), &k);
     GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)g.width * g.height), false, (cudaStream_t)stream, i > 0));
     const_cast<glint_ctx*>(c)->launches++;
     ++i;
@@ -479,11 +478,11 @@ static int host_pipeline_enqueue(glint_ctx* c, int n, const glint_gbuffer* gbs, 
       sub.pitch = W;
       sub.x0 = 0;
       sub.y0 = 0;
-      std::vector<unsigned long long*> slot;
-      int rc = sched_slots(c, s, 1, slot);
+      Slots slot;
+      const int rc = sched_slots(c, s, 1, &slot);
       if (rc) return rc;
       glint::KParams k;
-      make_params(c, &sub, &scs[f], c->d_stage[b][5], W, nullptr, slot[0], &k);
+      make_params(c, &sub, &scs[f], c->d_stage[b][5], W, nullptr, slot_at(c, slot, 0), &k);
       GL_CUDA(glint::launch_eval(k, grid_for(c, (int64_t)W * nr), false, s));
       c->launches++;
       GL_CUDA(cudaMemcpy2DAsync(out_tile + (int64_t)y0 * out_pitches[f], (size_t)out_pitches[f] * sizeof(float4),
