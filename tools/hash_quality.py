@@ -58,6 +58,12 @@ def rotr(t, k):
 
 def cand(name, hs, ka):
     """-> (y: gate word (bits 9..31), q: quantile index 0..4095)."""
+    if name.startswith("rotm"):          # rotm:a:j -- u = t ^ (rotr(t,a) & ~(1 << j)): 2 ops, a bijection for odd a
+        _, a, j = name.split(":")[:3]
+        t = ((hs + ka) & M) * C1 & M
+        u = t ^ (rotr(t, int(a)) & (M ^ U(1 << int(j))))
+        y = (u * C2) & M
+        return y, ((y ^ (y >> U(16))) >> U(2)) & U(4095)
     if name.startswith("rot3"):          # rot3:a:b -- t = x*C1; u = t ^ rotr(t,a) ^ rotr(t,b); y = u*C2 (bijective)
         _, a, b = name.split(":")[:3]
         t = ((hs + ka) & M) * C1 & M
@@ -114,7 +120,7 @@ def battery(name, n, cells, seed=0):
                 gb = ((ys[b] >> U(9)) < U(1 << 21)).astype(float)
                 corr_g.append(abs(np.corrcoef(ga, gb)[0, 1]))
                 corr_q.append(abs(np.corrcoef(z[qs[a].astype(np.int64)], z[qs[b].astype(np.int64)])[0, 1]))
-    return dict(ops=OPS.get(name, 6 if not name.endswith(':u') else 5), worst_chi2_p=worst_p, max_corr_gate=float(max(corr_g)),
+    return dict(ops=OPS.get(name, 5 if name.startswith('rotm') else (6 if not name.endswith(':u') else 5)), worst_chi2_p=worst_p, max_corr_gate=float(max(corr_g)),
                 max_corr_quantile=float(max(corr_q)), pairs=len(corr_g))
 
 
