@@ -552,6 +552,10 @@ def run_ours(args):
         ev, t = time_oracle(subs)
         cpu = {"value": ev / t, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
                "sample": f"{sample} ({ev} active evals, {t:.1f} s wall, {t * host_cores():.0f} core-s)"}
+        # the single-core figure beside the all-core one (the first frame's part of the sample)
+        ev1, t1 = time_oracle(subs[:1], threads=1)
+        cpu["value_1core"] = ev1 / t1
+        cpu["sample_1core"] = f"the first frame's bands of the sample, 1 thread ({ev1} active evals, {t1:.1f} s)"
 
     if rank == 0:
         line = {

@@ -109,9 +109,9 @@ def _tile_worker(rank, world, port, n_frames, q, band_rows=16):
         q.put((rank, repr(e), None))
 
 
-@pytest.mark.parametrize("world,n_frames", [(2, 1), (2, 3), (4, 1), (4, 3)])
+@pytest.mark.parametrize("world,n_frames", [(2, 1), (2, 3), (4, 1), (4, 3), (8, 1)])
 def test_gloo_tile_gather_assembles_the_single_rank_image(world, n_frames):
-    """SURVEY 8e at world sizes 2 and 4 on CPU: one frame cut into bands (C2 /
+    """SURVEY 8e at world sizes 2, 4 and 8 on CPU: one frame cut into bands (C2 /
     C3-style row-band sharding) or three frames (whole frames at 2 ranks,
     bands of every frame at 4: fewer frames than ranks), each tile shaded by its rank
     (the oracle stands in for the kernel) and gathered to rank 0 by the
@@ -121,7 +121,7 @@ def test_gloo_tile_gather_assembles_the_single_rank_image(world, n_frames):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    band = 8 if world == 4 else 16
+    band = {2: 16, 4: 8, 8: 4}[world]
     ps = [ctx.Process(target=_tile_worker, args=(r, world, port, n_frames, q, band)) for r in range(world)]
     for p in ps:
         p.start()
