@@ -470,6 +470,9 @@ def run_ours(args):
     roofline = {
         "bound": "alu", "achieved": achieved, "peak": issue_peak, "unit": "thread-inst/s",
         "frac": achieved / issue_peak,
+        "frac_note": ("W is SURVEY 8d's dense-draw budget; the kernel skips the count work of warp-grids with no "
+                      "passing gate (exact: production == DEBUG bit for bit), so it issues fewer instructions than W "
+                      "per eval and issue_frac_warp is the measured issue-slot utilisation"),
         "traffic": (traffic_pp * px_per_launch) if traffic_pp else None,
         "peak_source": f"{sms} SMs x 128 lanes x sm_max_mhz {f_max / 1e6:.0f} ({peak_src} MEASURED_PEAKS.json)",
         "algorithmic_inst_per_eval": w_eval,

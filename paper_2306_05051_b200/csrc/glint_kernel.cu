@@ -36,6 +36,12 @@
 #define GL_ASSERT(c) ((void)0)
 #endif
 
+// production MODE 0: evaluate a grid's 12 gates before its counts and skip
+// the counts when no lane of the warp passes (0 = the dense loop, for A/B)
+#ifndef GLINT_GATE_FIRST
+#define GLINT_GATE_FIRST 1
+#endif
+
 namespace glint {
 
 // ---------------------------------------------------------------------------
@@ -727,6 +733,28 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         rc->m1[i] = none ? 1.0f : gt.m1;
         rc->cap[i] = none ? 1.0f : gt.cap;
       }
+#if GLINT_GATE_FIRST
+      // gates first (production): a grid none of whose 12 x 32 lane-draws
+      // passes its gate adds nothing, so its counts (quantile load, clamp,
+      // floor, accumulate) are skipped by a warp vote. Glints are sparse: on
+      // C2 / C4 only 20-50 % of the warp-grids have a passing draw. The hash
+      // is recomputed below for the grids that pass (cheaper than keeping
+      // 12 words live). Results unchanged (production == DEBUG tests).
+      if (!DEBUG) {
+        bool pass = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+#pragma unroll
+          for (int jn = 0; jn < 4; ++jn) {
+            uint32_t y = hsC[i * 3 + k] + kaC[jn];
+            y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
+            y *= 0x846ca68bU;
+            pass = pass || (y <= G);
+          }
+        }
+        if (!__any_sync(am, pass && gt.T != 0u)) continue;
+      }
+#endif
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float bk = beta[i * 3 + k];

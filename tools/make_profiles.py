@@ -13,7 +13,7 @@ import sys
 
 args = sys.argv[1:]
 opts = {}
-for k in ("--pix", "--json", "--launch"):
+for k in ("--pix", "--json", "--launch", "--skip"):
     if k in args:
         i = args.index(k)
         opts[k] = args[i + 1]
@@ -85,7 +85,7 @@ os.makedirs("profiles", exist_ok=True)
 with open(OUT_JSON, "w") as fh:
     json.dump(summary, fh, indent=1)
 lines = [f"# ncu summary `{tag}` ({os.path.basename(rep)})", "",
-         "Captured with `ncu --set full --clock-control none --import-source on -k regex:glint_eval_kernel -s 3 -c 1`",
+         "Captured with `ncu --set full --clock-control none --import-source on -k regex:glint_eval_kernel -s " + opts.get("--skip", "3") + " -c 1` (tools/gpu/r2_full.sh)",
          f"on {LAUNCH}.", "",
          "| metric | value |", "|---|---|"]
 for k, val in summary.items():
