@@ -141,24 +141,32 @@ struct Gate {
   uint32_t T;
   float sigma, m1, cap;
 };
-__device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
+// the gate threshold T alone (what the gate phase of the draws needs)
+__device__ __forceinline__ uint32_t gate_T(float n, float p, float L2) {
   // L2 = log2(1 - p) for p in (0,1) and -inf for p = 1 (then exp2c(n L2) = 0
   // and P>=1 = 1 with no select), precomputed once per (pixel, light);
   // branch-free. For n <= 0 or p <= 0 only T needs forcing (to 0): the
   // sigma / m1 / cap of such a grid are never used (its count is 0), and
   // the DEBUG record reports the contract's values (0, 1, 1) explicitly.
-  Gate g;
   const bool none = !(n > 0.0f) || !(p > 0.0f);
   const float pge1 = 1.0f - exp2c(n * L2);
   const uint32_t T = __float2uint_ru(pge1 * 0x1p23f);   // = (uint32_t)ceil(P>=1 2^23), exact
+  return none ? 0u : T;
+}
+// the count parameters sigma, m1, cap (needed only when some draw passes)
+__device__ __forceinline__ void gate_counts(float n, float p, Gate& g) {
   const float nm1 = n - 1.0f;
   const float mu = nm1 > 0.0f ? nm1 * p : 0.0f;
   const float var = mu * (1.0f - p);
-  g.T = none ? 0u : T;
   const float rv = rsqrt_c(fmaxf(var, 0x1p-126f));          // always computed: no branch
   g.sigma = var >= 0x1p-126f ? var * rv : 0.0f;              // contract sqrt (subnormal -> 0)
   g.m1 = 1.0f + mu;
   g.cap = ceilf(n);
+}
+__device__ __forceinline__ Gate gate_params(float n, float p, float L2) {
+  Gate g;
+  g.T = gate_T(n, p, L2);
+  gate_counts(n, p, g);
   return g;
 }
 

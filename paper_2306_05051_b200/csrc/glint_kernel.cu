@@ -721,9 +721,33 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       // share their grid structure, so skip it when the whole warp agrees
       // (results unchanged)
       if (!DEBUG && !__any_sync(am, n[i] > 0.0f && p > 0.0f)) continue;
-      const Gate gt = gate_params(n[i], p, L2);
       // gate (y >> 9) < T  <=>  y <= T*512 - 1; T = 0 wraps to "always" but its
       // cap is forced to 0 so the count is 0 (same result, one compare)
+      Gate gt;
+      if (DEBUG || !GLINT_GATE_FIRST) {
+        gt = gate_params(n[i], p, L2);
+      } else {
+        // gates first (production): a grid none of whose 12 x 32 lane-draws
+        // passes its gate adds nothing, so its count work (sigma / m1 / cap,
+        // quantile load, clamp, floor, accumulate) is skipped by a warp vote.
+        // Glints are sparse: on C2 / C4 only 20-50 % of the warp-grids have
+        // a passing draw. Results unchanged (production == DEBUG tests).
+        gt.T = gate_T(n[i], p, L2);
+        const uint32_t Gg = (gt.T << 9) - 1u;
+        bool pass = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+#pragma unroll
+          for (int jn = 0; jn < 4; ++jn) {
+            uint32_t y = hsC[i * 3 + k] + kaC[jn];
+            y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
+            y *= 0x846ca68bU;
+            pass = pass || (y <= Gg);
+          }
+        }
+        if (!__any_sync(am, pass && gt.T != 0u)) continue;
+        gate_counts(n[i], p, gt);
+      }
       const uint32_t G = (gt.T << 9) - 1u;
       const float capk = gt.T ? gt.cap : 0.0f;
       if (DEBUG) {
@@ -733,28 +757,6 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         rc->m1[i] = none ? 1.0f : gt.m1;
         rc->cap[i] = none ? 1.0f : gt.cap;
       }
-#if GLINT_GATE_FIRST
-      // gates first (production): a grid none of whose 12 x 32 lane-draws
-      // passes its gate adds nothing, so its counts (quantile load, clamp,
-      // floor, accumulate) are skipped by a warp vote. Glints are sparse: on
-      // C2 / C4 only 20-50 % of the warp-grids have a passing draw. The hash
-      // is recomputed below for the grids that pass (cheaper than keeping
-      // 12 words live). Results unchanged (production == DEBUG tests).
-      if (!DEBUG) {
-        bool pass = false;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-#pragma unroll
-          for (int jn = 0; jn < 4; ++jn) {
-            uint32_t y = hsC[i * 3 + k] + kaC[jn];
-            y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
-            y *= 0x846ca68bU;
-            pass = pass || (y <= G);
-          }
-        }
-        if (!__any_sync(am, pass && gt.T != 0u)) continue;
-      }
-#endif
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         const float bk = beta[i * 3 + k];
