@@ -695,12 +695,29 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         const uint32_t key = ((uint32_t)als[g] & 511u) | ((uint32_t)alr[g] << 9) | ((uint32_t)ajo[g] << 13);
         const uint32_t base = so + key * 0x9e3779b1U + ix * 0x8da6b343U + iy * 0xd8163841U;
         const uint32_t lin[4] = {base, base + 0x8da6b343U, base + 0xd8163841U, base + (0x8da6b343U + 0xd8163841U)};
+        uint32_t hC[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) hC[k] = lowbias32(lin[k]) * c1s;
+        if (!DEBUG && GLINT_GATE_FIRST) {
+          // gates before counts, as for the method's 48 draws (a fair ablation)
+          bool pass = false;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+#pragma unroll
+            for (int jn = 0; jn < 4; ++jn) {
+              uint32_t y = hC[k] + kaC[jn];
+              y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
+              y *= 0x846ca68bU;
+              pass = pass || (y <= G);
+            }
+          }
+          if (!__any_sync(__activemask(), pass && gt.T != 0u)) continue;
+        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const uint32_t hC = lowbias32(lin[k]) * c1s;
 #pragma unroll
           for (int jn = 0; jn < 4; ++jn) {
-            uint32_t y = hC + kaC[jn];
+            uint32_t y = hC[k] + kaC[jn];
             y ^= __funnelshift_r(y, y, 11) ^ __funnelshift_r(y, y, 19);
             y *= 0x846ca68bU;
             const uint32_t s16 = y >> 16;
