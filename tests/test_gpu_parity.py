@@ -665,14 +665,19 @@ def test_intense_lights_near_the_surface(ctx):
 @pytest.mark.timeout(600)
 def test_full_size_production_equals_debug(ctx):
     """The bench's instantiation at full size: a whole 1920x1080 C2 frame (35
-    deg) and a 4K-wide C4 band (16 lights) give the same bits from the
-    production kernel (grid skips by warp vote, warp-uniform radiance) as from
-    the DEBUG kernel (every draw, per-lane radiance); the DEBUG records of
-    sampled pixels equal the oracle's."""
+    deg), a 4K-wide C4 band (16 lights) and 4K-wide C5 bands of the nearest,
+    middle and farthest frames (0 %, ~25 % and ~99 % of the warp-grids with a
+    passing draw: the gates-before-counts skip from never to always taken)
+    give the same bits from the production kernel (grid skips by warp vote,
+    gates before counts, warp-uniform radiance) as from the DEBUG kernel
+    (every draw, per-lane radiance); the DEBUG records of sampled pixels equal
+    the oracle's."""
     import oracle
     import paper_2306_05051_b200 as pkg
     from paper_2306_05051_b200 import synth
-    for fr in (synth.c2(35, device="cuda"), synth.c4(5, window=(900, 1156, 0, 3840), device="cuda")):
+    frames = [synth.c2(35, device="cuda"), synth.c4(5, window=(900, 1156, 0, 3840), device="cuda")]
+    frames += [synth.c5(f, window=(880, 1280, 0, 3840), device="cuda") for f in (0, 31, 63)]
+    for fr in frames:
         prod = pkg.glint_eval(ctx, fr.gbuf, fr.scene)
         dbg, rec = pkg.glint_eval(ctx, fr.gbuf, fr.scene, debug=True)
         torch.cuda.synchronize()
