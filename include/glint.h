@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define GLINT_VERSION 20000 /* 2.0.0: tile origin in glint_gbuffer, glint_count_active */
+#define GLINT_VERSION 20100 /* 2.1.0: debug record 184 words (simplex / angular fractions, P>=1); 2.0.0: tile origin, glint_count_active */
 
 /* return codes */
 #define GLINT_OK 0
@@ -133,7 +133,7 @@ typedef struct {
                        place in a full-frame output (local, or a peer GPU's mapped buffer) */
 } glint_gbuffer;
 
-/* Optional per (pixel, light) debug record (168 words, 672 bytes), written
+/* Optional per (pixel, light) debug record (184 words, 736 bytes), written
  * in-kernel by the same arithmetic (template instantiation) when `dbg` is
  * non-NULL; record index = (y * width + x) * n_lights + light. For tiny
  * parity inputs only. Fields mirror DESIGN.md §4.3. */
@@ -152,7 +152,10 @@ typedef struct {
   float Dp;                        /* S8 D_P(h) */
   uint32_t flags;
   uint32_t light_active;           /* n.wi > 0 and n.wo > 0 */
-  uint32_t reserved[2];
+  float sfx[4], sfy[4];            /* S3 simplex cell fractions per slot (beta = barycentrics of (sfx, sfy)) */
+  float afx, afy;                  /* S5 angular cell fractions (v_j = their bilinear weights, Eq. 14) */
+  float pge1[4];                   /* S6 P>=1 = 1 - (1-p)^n per slot (0 when n <= 0 or p <= 0) */
+  uint32_t reserved[4];
 } glint_debug_rec;
 
 int glint_version(void);

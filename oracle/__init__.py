@@ -63,9 +63,10 @@ REC_DTYPE = np.dtype([
     ("p", "<f4"), ("cx0", "<i4"), ("cy0", "<i4"),
     ("T", "<u4", 4), ("sigma", "<f4", 4), ("m1", "<f4", 4), ("cap", "<f4", 4),
     ("hash", "<u4", 48), ("count", "<f4", 48),
-    ("C", "<f4"), ("Dp", "<f4"), ("flags", "<u4"), ("light_active", "<u4"), ("pad_", "<u4", 2),
+    ("C", "<f4"), ("Dp", "<f4"), ("flags", "<u4"), ("light_active", "<u4"), 
+    ("sfx", "<f4", 4), ("sfy", "<f4", 4), ("afx", "<f4"), ("afy", "<f4"), ("pge1", "<f4", 4), ("pad_", "<u4", 4),
 ])
-assert REC_DTYPE.itemsize == 168 * 4
+assert REC_DTYPE.itemsize == 184 * 4
 
 _lib = None
 _lock = threading.Lock()

@@ -451,15 +451,17 @@ void orc_bilinear(float x, float y, int64_t lx[4], int64_t ly[4], float beta[4])
  * bits as h) and T = ceil(P>=1 2^23); z = Z[(h >> 2) & 4095] (bits 2..13);
  * count = floor(clamp(1 + mu + sigma z, 1, ceil(n))) (reading R-3).         */
 /* ---------------------------------------------------------------------- */
+/* P>=1 = 1 - (1-p)^n (Eq. 16) for n > 0, p > 0; 0 otherwise (no trials) */
+static float pge1_of(float n, float p) {
+  if (!(n > 0.0f) || !(p > 0.0f)) return 0.0f;
+  if (p >= 1.0f) return 1.0f;
+  float y = n * orc_log2_1mp(p);        /* log2((1-p)^n) */
+  return 1.0f - orc_exp2(y);            /* Eq. 16 */
+}
+
 void orc_gate_params(float n, float p, uint32_t* T, float* sigma, float* m1, float* cap) {
   if (!(n > 0.0f) || !(p > 0.0f)) { *T = 0; *sigma = 0.0f; *m1 = 1.0f; *cap = 1.0f; return; }
-  float Pge1;
-  if (p >= 1.0f) {
-    Pge1 = 1.0f;
-  } else {
-    float y = n * orc_log2_1mp(p);      /* log2((1-p)^n) */
-    Pge1 = 1.0f - orc_exp2(y);          /* Eq. 16 */
-  }
+  float Pge1 = pge1_of(n, p);
   *T = (uint32_t)ceilf(Pge1 * 0x1p23f);
   float nm1 = n - 1.0f;
   float mu = nm1 > 0.0f ? nm1 * p : 0.0f; /* Eq. 17 (R-4: n < 1 -> mu = 0) */
@@ -805,6 +807,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
   uint32_t hs[10][4];
   int64_t lxs[10][4], lys[10][4];
   double betad[10][4];
+  float sfx[4] = {0, 0, 0, 0}, sfy[4] = {0, 0, 0, 0};   /* simplex fractions (records) */
   for (int i = 0; i < NG; ++i) {
     float x, y, be[4];
     orc_grid_uv(u, v, ls[i], lr[i], jo[i], &x, &y);
@@ -813,6 +816,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       /* barycentrics recomputed in fp64 from the exact fp32 fractions */
       float xs = x + 0.5f * y;
       double fx = (double)(xs - floorf(xs)), fy = (double)(y - floorf(y));
+      sfx[i] = (float)fx; sfy[i] = (float)fy;
       if (fx >= fy) { betad[i][0] = 1.0 - fx; betad[i][1] = fx - fy; betad[i][2] = fy; }
       else          { betad[i][0] = 1.0 - fy; betad[i][1] = fy - fx; betad[i][2] = fx; }
     } else {
@@ -849,6 +853,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       rc->P = P; rc->r = r; rc->psi = psi;
       for (int i = 0; i < 4; ++i) { rc->ls[i] = ls[i]; rc->lr[i] = lr[i]; rc->jo[i] = jo[i]; rc->w[i] = w[i]; rc->n[i] = n[i]; }
       for (int i = 0; i < 4; ++i) for (int k = 0; k < 3; ++k) { rc->lx[i*3+k] = (int32_t)(uint32_t)lxs[i][k]; rc->ly[i*3+k] = (int32_t)(uint32_t)lys[i][k]; }
+      for (int i = 0; i < 4; ++i) { rc->sfx[i] = sfx[i]; rc->sfy[i] = sfy[i]; }
     }
     /* S5: light direction d toward the light (P:L1228 punctual lights only,
      * reading R-27); w_o = d/|d|. The light is active iff n.w_i > 0 and
@@ -881,7 +886,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
       uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
       ka[jn] = orc_lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
     }
-    if (rc) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
+    if (rc) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; rc->afx = (float)fxa; rc->afy = (float)fya; }
 
     /* S6 + S7 + S8: 4 grids x 3 spatial x 4 angular = 48 draws
      * (ablations: 4 x 4 x 4 = 64; 10 x 4 x 4 = 160) */
@@ -889,7 +894,7 @@ static void eval_pixel(const float duv[4], const float uvm[4], const float nrm[4
     for (int i = 0; i < NG; ++i) {
       uint32_t T; float sig, m1, cap;
       orc_gate_params(n[i], p, &T, &sig, &m1, &cap);
-      if (rc) { rc->T[i] = T; rc->sigma[i] = sig; rc->m1[i] = m1; rc->cap[i] = cap; }
+      if (rc) { rc->T[i] = T; rc->sigma[i] = sig; rc->m1[i] = m1; rc->cap[i] = cap; rc->pge1[i] = pge1_of(n[i], p); }
       double Ci = 0.0; /* b_theta_i(w_i N_i, p), interpolated (Eq. 14, R-16) */
       for (int k = 0; k < NS; ++k) {
         double Cik = 0.0;

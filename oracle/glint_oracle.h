@@ -53,7 +53,7 @@ typedef struct {
   orc_light lights[ORC_MAX_LIGHTS];
 } orc_scene;
 
-/* per (pixel, light) debug record -- 168 x 4-byte words */
+/* per (pixel, light) debug record -- 184 x 4-byte words */
 typedef struct {
   float P, r, psi;                 /* footprint (S1) */
   int32_t ls[4], lr[4], jo[4];     /* 4 lattice slots (S2) */
@@ -69,7 +69,10 @@ typedef struct {
   float Dp;                        /* D_P(h) (Eq. 3), fp32 view */
   uint32_t flags;
   uint32_t light_active;           /* 1 if n.wi > 0 and n.wo > 0 */
-  uint32_t pad_[2];
+  float sfx[4], sfy[4];            /* simplex cell fractions per grid (S3) */
+  float afx, afy;                  /* angular cell fractions (Eq. 14) */
+  float pge1[4];                   /* P>=1 per grid (Eq. 16; 0 if n <= 0 or p <= 0) */
+  uint32_t pad_[4];
 } orc_rec;
 
 int orc_init(void);

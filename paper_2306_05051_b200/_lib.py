@@ -54,7 +54,7 @@ class glint_gbuffer(C.Structure):
                 ("x0", C.c_int32), ("y0", C.c_int32)]
 
 
-# glint_debug_rec (168 words) as a numpy structured dtype
+# glint_debug_rec (184 words) as a numpy structured dtype
 DEBUG_REC_DTYPE = np.dtype([
     ("P", "<f4"), ("r", "<f4"), ("psi", "<f4"),
     ("ls", "<i4", 4), ("lr", "<i4", 4), ("jo", "<i4", 4),
@@ -63,9 +63,10 @@ DEBUG_REC_DTYPE = np.dtype([
     ("p", "<f4"), ("cx0", "<i4"), ("cy0", "<i4"),
     ("T", "<u4", 4), ("sigma", "<f4", 4), ("m1", "<f4", 4), ("cap", "<f4", 4),
     ("hash", "<u4", 48), ("count", "<f4", 48),
-    ("C", "<f4"), ("Dp", "<f4"), ("flags", "<u4"), ("light_active", "<u4"), ("reserved", "<u4", 2),
+    ("C", "<f4"), ("Dp", "<f4"), ("flags", "<u4"), ("light_active", "<u4"), 
+    ("sfx", "<f4", 4), ("sfy", "<f4", 4), ("afx", "<f4"), ("afy", "<f4"), ("pge1", "<f4", 4), ("reserved", "<u4", 4),
 ])
-DEBUG_REC_BYTES = 168 * 4
+DEBUG_REC_BYTES = 184 * 4
 assert DEBUG_REC_DTYPE.itemsize == DEBUG_REC_BYTES
 
 _lib = None

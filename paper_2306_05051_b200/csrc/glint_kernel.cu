@@ -498,6 +498,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
   uint32_t hsC[12];
   float beta[12];
   uint32_t dlx[DEBUG ? 12 : 1], dly[DEBUG ? 12 : 1], dhs[DEBUG ? 12 : 1];
+  float dfx[DEBUG ? 4 : 1] = {}, dfy[DEBUG ? 4 : 1] = {};
 #pragma unroll
   for (int i = 0; i < (MODE == 0 ? 4 : 0); ++i) {
     GL_ASSERT(sl[i].lr >= 0 && sl[i].lr <= 8 && sl[i].jo >= 0 && (sl[i].jo >> sl[i].lr) == 0);
@@ -527,6 +528,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     hsC[i * 3 + 1] = h1 * c1s;
     hsC[i * 3 + 2] = h2 * c1s;
     if (DEBUG) {
+      dfx[i] = fx; dfy[i] = fy;
       dlx[i * 3 + 0] = ix; dly[i * 3 + 0] = iy;
       dlx[i * 3 + 1] = lower ? ix + 1u : ix; dly[i * 3 + 1] = lower ? iy : iy + 1u;
       dlx[i * 3 + 2] = ix + 1u; dly[i * 3 + 2] = iy + 1u;
@@ -565,6 +567,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       rc->P = P; rc->r = r; rc->psi = psi;
       for (int i = 0; i < 4; ++i) { rc->ls[i] = sl[i].ls; rc->lr[i] = sl[i].lr; rc->jo[i] = sl[i].jo; rc->w[i] = sl[i].w; rc->n[i] = n[i]; }
       for (int q = 0; q < 12; ++q) { rc->lx[q] = (int32_t)dlx[q]; rc->ly[q] = (int32_t)dly[q]; }
+      for (int i = 0; i < 4; ++i) { rc->sfx[i] = dfx[i]; rc->sfy[i] = dfy[i]; }
     }
     // light below the horizon (R-27); |d|^2 a normal float (R-27b)
     if (!light_active(ni, nd, d2)) continue;
@@ -606,7 +609,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
       const uint32_t ka0 = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
       kaC[jn] = MODE == 3 ? ka0 : ka0 * c1n;
     }
-    if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; }
+    if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; rc->afx = fxa; rc->afy = fya; }
 
     // ---------------- S6 + S7 + S8: 48 gated draws, blended
     const float L2 = p >= 1.0f ? -__int_as_float(0x7f800000) : (p > 0.0f ? log2_1mp(p) : 0.0f);   // see gate_params
@@ -773,6 +776,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
         rc->sigma[i] = none ? 0.0f : gt.sigma;
         rc->m1[i] = none ? 1.0f : gt.m1;
         rc->cap[i] = none ? 1.0f : gt.cap;
+        rc->pge1[i] = none ? 0.0f : 1.0f - exp2c(n[i] * L2);   // gate_T's P>=1
       }
 #pragma unroll
       for (int k = 0; k < 3; ++k) {

@@ -27,7 +27,7 @@ def test_exports_match_header(glib):
     L = glib.lib()
     for name in declared:
         assert hasattr(L, name)
-    assert glib.version() == 20000
+    assert glib.version() == 20100
     assert glib.strerror(-1) == "invalid argument"
 
 

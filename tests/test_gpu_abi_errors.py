@@ -54,7 +54,7 @@ def test_error_codes(env):
     bad_out = torch.empty(32 * 64 * 4 + 1, device="cuda")[1:]                       # misaligned output
     assert L.lib().glint_eval(ctx.handle, C.byref(g), C.byref(sc), bad_out.data_ptr(), 64, None, None) == L.GLINT_EALIGN
     s2 = L.scene_struct(fr.scene); s2.eval_mode = 3                                  # debug records: mode 0 only
-    dbg = torch.empty(32 * 64 * 168 * 4, dtype=torch.uint8, device="cuda")
+    dbg = torch.empty(32 * 64 * L.DEBUG_REC_BYTES, dtype=torch.uint8, device="cuda")
     assert _call(L, ctx, g, s2, out, C.c_void_p(dbg.data_ptr())) == L.GLINT_EINVAL
     torch.cuda.synchronize()
     assert torch.all(out == 7.0)                                                    # untouched

@@ -11,8 +11,8 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-EXACT = ("P", "r", "psi", "ls", "lr", "jo", "w", "n", "lx", "ly", "p", "cx0", "cy0", "T", "sigma", "m1",
-         "cap", "hash", "count", "flags", "light_active")
+EXACT = ("P", "r", "psi", "ls", "lr", "jo", "w", "n", "lx", "ly", "sfx", "sfy", "p", "cx0", "cy0", "afx", "afy",
+         "T", "pge1", "sigma", "m1", "cap", "hash", "count", "flags", "light_active")
 RTOL = 1e-4
 
 
