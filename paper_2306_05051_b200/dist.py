@@ -175,15 +175,61 @@ class TileGather:
         return works
 
 
+LAST_MAPPING = None      # how this process last mapped a peer buffer (tests)
+
+
+class _DevicePointer:
+    """A device pointer seen through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr, shape, strides_bytes, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "strides": tuple(strides_bytes), "version": 3}
+
+
+def _ipc_open_here(args):
+    """Map rank ``src``'s exported allocation into this process from THIS
+    rank's device: cudaIpcOpenMemHandle with cudaIpcMemLazyEnablePeerAccess,
+    called with the rank's own device current, enables peer access from it to
+    the owner's device, which is what its kernels' stores need (torch's own
+    rebuild opens the handle from the owner's device, whose peer mapping the
+    rank's device would not have). Returns a tensor over the mapping, or None
+    when the handle is not a plain cudaMalloc export."""
+    (_cls, size, stride, toff, _scls, dtype, _sdev, handle, _sbytes, soff) = args[:10]
+    # torch's handle: [version byte (2)] + type byte ('c': cudaMalloc) + cudaIpcMemHandle_t
+    if len(handle) == 66 and handle[1:2] == b"c":
+        raw = handle[2:]
+    elif len(handle) == 65 and handle[:1] == b"c":
+        raw = handle[1:]
+    else:
+        raw = handle
+    if len(raw) != 64:
+        return None
+    from cuda.bindings import runtime as rt
+    dev = torch.cuda.current_device()
+    (err,) = rt.cudaSetDevice(dev)
+    if err != rt.cudaError_t.cudaSuccess:
+        raise RuntimeError(f"cudaSetDevice({dev}): {err}")
+    h = rt.cudaIpcMemHandle_t()
+    h.reserved = bytes(raw)
+    err, ptr = rt.cudaIpcOpenMemHandle(h, rt.cudaIpcMemLazyEnablePeerAccess)
+    if err != rt.cudaError_t.cudaSuccess:
+        raise RuntimeError(f"cudaIpcOpenMemHandle on device {dev}: {err}")
+    item = torch.empty((), dtype=dtype).element_size()
+    typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
+    base = int(ptr) + int(soff) + int(toff) * item
+    return torch.as_tensor(_DevicePointer(base, size, [st * item for st in stride], typestr))
+
+
 def peer_buffer(shape, dtype=torch.float32, device=None, src: int = 0):
     """One device buffer owned by rank ``src`` and mapped into every rank's
-    address space (CUDA IPC: cudaIpcGetMemHandle / cudaIpcOpenMemHandle with
-    lazy peer access, through torch's tensor-sharing reductions). A rank that
-    passes a slice of it as ``out`` to glint_eval has its kernel store the
-    radiance straight into rank ``src``'s HBM over NVLink: the gather to rank 0
-    becomes part of the shading kernel, overlapping it tile by tile, with no
-    separate collective. Returns the buffer (``src``) or its
-    mapping (others); the control plane only moves the IPC handle."""
+    address space (CUDA IPC: cudaIpcGetMemHandle on the owner, then
+    cudaIpcOpenMemHandle with lazy peer access from each rank's own device).
+    A rank that passes a slice of it as ``out`` to glint_eval has its kernel
+    store the radiance straight into rank ``src``'s HBM over NVLink: the
+    gather to rank 0 becomes part of the shading kernel, overlapping it tile
+    by tile, with no separate collective. Returns the buffer
+    (``src``) or its mapping (others); the control plane only moves the IPC
+    handle."""
     from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
     rank = dist.get_rank() if dist.is_initialized() else 0
     world = dist.get_world_size() if dist.is_initialized() else 1
@@ -198,5 +244,10 @@ def peer_buffer(shape, dtype=torch.float32, device=None, src: int = 0):
     if world > 1:
         dist.broadcast_object_list(obj, src=src)
         if rank != src:
-            buf = rebuild_cuda_tensor(*obj[0])
+            global LAST_MAPPING
+            buf = _ipc_open_here(obj[0])
+            LAST_MAPPING = "ipc-open on the rank's device"
+            if buf is None:       # not a plain cudaMalloc export: torch's own mapping
+                buf = rebuild_cuda_tensor(*obj[0])
+                LAST_MAPPING = "torch rebuild"
     return buf

@@ -1,6 +1,7 @@
 """The fused gather of SURVEY §8e on one GPU: two processes (gloo control
 plane, 127.0.0.1), rank 0 owns one buffer for all frames and maps it into
-rank 1 through CUDA IPC (dist.peer_buffer); each rank's kernel stores its
+rank 1 through CUDA IPC (dist.peer_buffer: the handle opened from rank 1's
+own device with lazy peer access, the path a multi-GPU rank takes); each rank's kernel stores its
 frames (f = rank mod 2) straight into that buffer. No kernel waits on another
 rank: rank 1 only writes, then a host barrier. Rank 0 then checks every frame
 bit for bit against its own local evaluation."""
@@ -35,6 +36,8 @@ def _worker(rank, world, port, q):
         ctx = pkg.Context(0)
         frames = [synth.c2(e, window=(500, 564, 0, 256), device="cuda") for e in (15, 35, 55, 75, 90)]
         buf = D.peer_buffer((len(frames), 64, 256, 4), device=torch.device("cuda", 0))
+        if rank == 1 and D.LAST_MAPPING != "ipc-open on the rank's device":
+            raise RuntimeError(f"peer buffer mapped by {D.LAST_MAPPING}")
         if rank == 0:
             buf.fill_(float("nan"))
             torch.cuda.synchronize()
