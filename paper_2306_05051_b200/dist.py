@@ -179,11 +179,22 @@ LAST_MAPPING = None      # how this process last mapped a peer buffer (tests)
 
 
 class _DevicePointer:
-    """A device pointer seen through __cuda_array_interface__ (no copy)."""
+    """A device pointer seen through __cuda_array_interface__ (no copy). The
+    tensor torch builds over it keeps this object alive; when the last view
+    goes, the IPC mapping ``mapped`` is closed."""
 
-    def __init__(self, ptr, shape, strides_bytes, typestr):
+    def __init__(self, ptr, shape, strides_bytes, typestr, mapped=None):
         self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
                                          "strides": tuple(strides_bytes), "version": 3}
+        self._mapped = mapped
+
+    def __del__(self):
+        if self._mapped is not None:
+            try:
+                from cuda.bindings import runtime as rt
+                rt.cudaIpcCloseMemHandle(self._mapped)
+            except Exception:     # interpreter shutdown: the process exit unmaps it
+                pass
 
 
 def _ipc_open_here(args):
@@ -217,7 +228,7 @@ def _ipc_open_here(args):
     item = torch.empty((), dtype=dtype).element_size()
     typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
     base = int(ptr) + int(soff) + int(toff) * item
-    return torch.as_tensor(_DevicePointer(base, size, [st * item for st in stride], typestr))
+    return torch.as_tensor(_DevicePointer(base, size, [st * item for st in stride], typestr, mapped=ptr))
 
 
 def peer_buffer(shape, dtype=torch.float32, device=None, src: int = 0):
