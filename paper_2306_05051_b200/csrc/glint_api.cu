@@ -48,6 +48,7 @@ struct glint_ctx {
   std::mutex host_mu;   // serialises glint_eval_host (staging and streams are per context)
 };
 
+static_assert(sizeof(glint_debug_rec) == 184 * 4, "glint.h 2.1: the debug record is 184 words");
 extern "C" int glint_version(void) { return GLINT_VERSION; }
 
 extern "C" const char* glint_strerror(int code) {
