@@ -46,3 +46,15 @@ def test_oracle_record_matches_its_header():
     offs = _c_offsets(os.path.join(ROOT, "oracle"), "glint_oracle.h", "orc_rec", dt.names)
     _check(dt, offs)
     assert offs["size"] == 184 * 4
+
+
+@pytest.mark.parametrize("name", ["glint_gbuffer", "glint_scene", "glint_light"])
+def test_ctypes_structs_match_glint_h(name):
+    from paper_2306_05051_b200 import _lib
+    import ctypes
+    st = getattr(_lib, name)
+    fields = [f[0] for f in st._fields_ if not f[0].startswith("pad")]
+    offs = _c_offsets(os.path.join(ROOT, "include"), "glint.h", name, fields)
+    assert offs["size"] == ctypes.sizeof(st)
+    for f in fields:
+        assert offs[f] == getattr(st, f).offset, f
