@@ -787,3 +787,26 @@ def test_radiance_shell_tiers(ctx, f0):
         compare_records(rec, rec_o, f"{fr.name} f0={f0}")
         compare_radiance(out, rgb_o, fl_o, f"{fr.name} f0={f0}")
         assert rgb_o.max() > 0
+
+
+def test_pixel_order_does_not_change_any_result(ctx):
+    """Every (pixel, light) evaluation is a pure function of its G-buffer
+    entry, the scene and the seed (the basis of tile sharding, SURVEY 8e, and
+    of the warp-shape probe): shading a frame with its
+    pixels permuted in memory (random permutation, and 8x4 warp blocks) gives
+    the permuted output bit for bit, though every warp then holds other
+    pixels (other vote outcomes, other skipped grids)."""
+    import paper_2306_05051_b200 as pkg
+    from paper_2306_05051_b200 import synth
+    fr = synth.c5(40, window=(900, 964, 0, 512), device="cuda")
+    ref = pkg.glint_eval(ctx, fr.gbuf, fr.scene).reshape(-1, 4)
+    H, W = fr.gbuf.height, fr.gbuf.width
+    g = torch.Generator().manual_seed(7)
+    perms = [torch.randperm(H * W, generator=g),
+             torch.arange(H * W).reshape(H // 4, 4, W // 8, 8).permute(0, 2, 1, 3).reshape(-1)]
+    for perm in perms:
+        pd = perm.to("cuda")
+        planes = [p.reshape(-1, 4)[pd].reshape(-1, 256, 4).contiguous() for p in fr.gbuf.planes()]
+        out = pkg.glint_eval(ctx, synth.GBuffer(*planes), fr.scene).reshape(-1, 4)
+        torch.cuda.synchronize()
+        assert torch.equal(out.view(torch.int32), ref[pd].view(torch.int32))
