@@ -41,6 +41,11 @@
 #ifndef GLINT_GATE_FIRST
 #define GLINT_GATE_FIRST 1
 #endif
+// production MODE 0-2: angular node seeds from a per-launch shared-memory
+// table (0 = computed per pixel-light, for A/B)
+#ifndef GLINT_KA_TABLE
+#define GLINT_KA_TABLE 1
+#endif
 
 namespace glint {
 
@@ -392,6 +397,11 @@ __device__ __forceinline__ bool radiance_shell32(const glint_scene& sc, int ndf,
 // quantile lookup in the draw loop is a single LDS with an immediate base
 __shared__ __align__(128) float g_sZ[GLINT_ZQ];
 __shared__ __align__(16) float2 g_sCS[GLINT_NANG];
+// angular node seeds ka(cx, cy) * C1 of every node a pixel-light can reach
+// (|h_x|, |h_y| <= 1: cx in [-ceil(1/beta) - 2, ceil(1/beta) + 2]), built per
+// launch by each block: four LDS per pixel-light instead of four lowbias32.
+// Same values as the direct computation (production == DEBUG tests).
+__shared__ __align__(16) uint32_t g_sKA[kKaMax];
 
 // ---------------------------------------------------------------------------
 // Shading of one pixel (S1..S9). Inputs already in registers; `outp` is the
@@ -405,7 +415,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
                                             uint32_t seed_h, float inv_beta, uint32_t c1s, uint32_t c1n,
-                                            bool f0_fast) {
+                                            bool f0_fast, int ka_lo, int ka_n) {
   const int ndf = NDF >= 0 ? NDF : sc.ndf_kind;
   const int L = sc.n_lights;
   uint32_t flags = 0;
@@ -603,11 +613,18 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const int cx0 = (int)cxf, cy0 = (int)cyf;
     const float vj[4] = {(1.0f - fxa) * (1.0f - fya), fxa * (1.0f - fya), (1.0f - fxa) * fya, fxa * fya};
     uint32_t kaC[4];
+    const uint32_t kix = (uint32_t)(cx0 - ka_lo), kiy = (uint32_t)(cy0 - ka_lo);
+    if (!DEBUG && MODE != 3 && GLINT_KA_TABLE && ka_n > 0 && kix < (uint32_t)(ka_n - 1) && kiy < (uint32_t)(ka_n - 1)) {
+      const int e = (int)kiy * ka_n + (int)kix;
+      GL_ASSERT(e >= 0 && e + ka_n + 1 < kKaMax);
+      kaC[0] = g_sKA[e]; kaC[1] = g_sKA[e + 1]; kaC[2] = g_sKA[e + ka_n]; kaC[3] = g_sKA[e + ka_n + 1];
+    } else {
 #pragma unroll
-    for (int jn = 0; jn < 4; ++jn) {
-      const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
-      const uint32_t ka0 = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
-      kaC[jn] = MODE == 3 ? ka0 : ka0 * c1n;
+      for (int jn = 0; jn < 4; ++jn) {
+        const uint32_t cx = (uint32_t)(cx0 + (jn & 1)), cy = (uint32_t)(cy0 + (jn >> 1));
+        const uint32_t ka0 = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU);
+        kaC[jn] = MODE == 3 ? ka0 : ka0 * c1n;
+      }
     }
     if (DEBUG) { rc->p = p; rc->cx0 = cx0; rc->cy0 = cy0; rc->afx = fxa; rc->afy = fya; }
 
@@ -863,6 +880,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   const float inv_beta = 1.0f / sc.beta;
   const uint32_t seed_h = lowbias32(sc.seed);
   const bool flat_out = prm.out_pitch == prm.width;
+  // node-seed table extent: cx, cy in [ka_lo, ka_lo + ka_n) (ka_n = 0: none)
+  int ka_lo = 0, ka_n = 0;
+  if (!DEBUG && MODE != 3 && GLINT_KA_TABLE && inv_beta <= 29.0f) {
+    const int cb = (int)ceilf(inv_beta);
+    ka_lo = -cb - 2;
+    ka_n = 2 * cb + 5;
+  }
 
   auto issue = [&](int64_t t, int b) {   // one thread: tile t into stage b (or just its id)
     s_tile[b] = t;
@@ -899,7 +923,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
     issue(blockIdx.x, 0);
     for (int s = 1; s < kStages; ++s) issue(any ? claim() : n_tiles, s);
   }
-  __syncthreads();   // barriers initialised
+  for (int e = tid; e < ka_n * ka_n; e += kBlock) {   // node-seed table (same arithmetic as S5's)
+    const int iy = e / ka_n, ix = e - iy * ka_n;
+    const uint32_t cx = (uint32_t)(ka_lo + ix), cy = (uint32_t)(ka_lo + iy);
+    g_sKA[e] = lowbias32(cx * 0xcb1ab31fU + cy * 0x165667b1U + 0x27d4eb2fU) * prm.c1n;
+  }
+  __syncthreads();   // barriers initialised, node-seed table built
   mbar_wait(tbar, 0u);
 
   for (int it = 0;; ++it) {
@@ -932,7 +961,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
                 oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
       shade_pixel<DEBUG, MODE, NDF>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
-                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0);
+                               nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0, ka_lo, ka_n);
     }
     __syncwarp();
     if (lane == 0) {

@@ -29,6 +29,7 @@ constexpr int kSchedSlots = 1024;               // per-context ring of per-launc
 constexpr int kCaptureSlots = 4096;             // per-context pool for graph-captured launches (never recycled)
 constexpr size_t kSmemZ = GLINT_ZQ * sizeof(float);             // 16 KB quantile table
 constexpr size_t kSmemCS = GLINT_NANG * sizeof(float2);         // 2 KB orientation table
+constexpr int kKaMax = 4096;   // angular node-seed table: up to 64 x 64 nodes (16 KB; beta >= ~1/30)
 constexpr size_t kSmemTables = 256;    // dynamic part: table + kStages mbarriers, tile ids, counters (padded)
 static_assert(8 * (1 + kStages) + 8 * kStages + 4 * kStages <= kSmemTables, "barrier area");
 constexpr size_t kSmemTma = kSmemTables + (size_t)kStages * 5 * kTile * 16;  // + kStages x 5 planes x kTile float4
