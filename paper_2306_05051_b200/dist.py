@@ -215,7 +215,10 @@ def _ipc_open_here(args):
         raw = handle
     if len(raw) != 64:
         return None
-    from cuda.bindings import runtime as rt
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:   # no cuda-python: torch's own mapping (same-device ranks only)
+        return None
     dev = torch.cuda.current_device()
     (err,) = rt.cudaSetDevice(dev)
     if err != rt.cudaError_t.cudaSuccess:
