@@ -41,8 +41,8 @@
 #ifndef GLINT_GATE_FIRST
 #define GLINT_GATE_FIRST 1
 #endif
-// production MODE 0-2: angular node seeds from a per-launch shared-memory
-// table (0 = computed per pixel-light, for A/B)
+// production MODE 0-2 with several lights: angular node seeds from a
+// per-launch shared-memory table (0 = computed per pixel-light, for A/B)
 #ifndef GLINT_KA_TABLE
 #define GLINT_KA_TABLE 1
 #endif
@@ -410,7 +410,7 @@ __shared__ __align__(16) uint32_t g_sKA[kKaMax];
 // NDF: the scene's ndf_kind fixed at compile time (0 GGX, 1 Beckmann) for the
 // production kernel of the method, -1 = read from the scene (DEBUG, ablations,
 // baseline): the GGX / Beckmann branches of S5 and of the shell disappear
-template <bool DEBUG, int MODE, int NDF>
+template <bool DEBUG, int MODE, int NDF, bool KAT>
 __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* __restrict__ sZ,
                                             const float2* __restrict__ sCS, float4* outp, glint_debug_rec* rec,
                                             float4 duv, float4 uvm, float4 nrm, float4 pos, float4 mat,
@@ -614,7 +614,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
     const float vj[4] = {(1.0f - fxa) * (1.0f - fya), fxa * (1.0f - fya), (1.0f - fxa) * fya, fxa * fya};
     uint32_t kaC[4];
     const uint32_t kix = (uint32_t)(cx0 - ka_lo), kiy = (uint32_t)(cy0 - ka_lo);
-    if (!DEBUG && MODE != 3 && GLINT_KA_TABLE && ka_n > 0 && kix < (uint32_t)(ka_n - 1) && kiy < (uint32_t)(ka_n - 1)) {
+    if (KAT && ka_n > 0 && kix < (uint32_t)(ka_n - 1) && kiy < (uint32_t)(ka_n - 1)) {
       const int e = (int)kiy * ka_n + (int)kix;
       GL_ASSERT(e >= 0 && e + ka_n + 1 < kKaMax);
       kaC[0] = g_sKA[e]; kaC[1] = g_sKA[e + 1]; kaC[2] = g_sKA[e + ka_n]; kaC[3] = g_sKA[e + ka_n + 1];
@@ -862,7 +862,7 @@ __device__ __forceinline__ void shade_pixel(const glint_scene& sc, const float* 
 // barrier inside the loop; a warp can run up to kStages - 1 tiles ahead of
 // the slowest one. Without TMA the ring carries only tile ids.
 // ---------------------------------------------------------------------------
-template <bool DEBUG, bool TMA, int MODE, int NDF>
+template <bool DEBUG, bool TMA, int MODE, int NDF, bool KAT>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KParams prm) {
   float* sZ = g_sZ;
   float2* sCS = g_sCS;
@@ -882,7 +882,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   const bool flat_out = prm.out_pitch == prm.width;
   // node-seed table extent: cx, cy in [ka_lo, ka_lo + ka_n) (ka_n = 0: none)
   int ka_lo = 0, ka_n = 0;
-  if (!DEBUG && MODE != 3 && GLINT_KA_TABLE && inv_beta <= 29.0f) {
+  if (KAT && inv_beta <= 29.0f) {
     const int cb = (int)ceilf(inv_beta);
     ka_lo = -cb - 2;
     ka_n = 2 * cb + 5;
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
       }
       GL_ASSERT(idx >= 0 && idx < n_pix && oi >= 0 &&
                 oi < (int64_t)(prm.height - 1) * prm.out_pitch + prm.width && slot < kTile);
-      shade_pixel<DEBUG, MODE, NDF>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
+      shade_pixel<DEBUG, MODE, NDF, KAT>(sc, sZ, sCS, prm.out + oi, DEBUG ? prm.dbg + idx * sc.n_lights : nullptr, duv, uvm,
                                nrm, pos, mat, seed_h, inv_beta, prm.c1s, prm.c1n, prm.f0_fast != 0, ka_lo, ka_n);
     }
     __syncwarp();
@@ -990,7 +990,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) glint_eval_kernel(const KP
   }
 }
 
-template <bool DEBUG, bool TMA, int MODE, int NDF = -1>
+template <bool DEBUG, bool TMA, int MODE, int NDF = -1, bool KAT = false>
 static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, bool pdl) {
   const size_t smem = TMA ? kSmemTma : kSmemTables;
   // the dynamic shared-memory opt-in, once per (instantiation, device);
@@ -1002,13 +1002,13 @@ static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, b
   if (e != cudaSuccess) return e;
   const uint64_t bit = 1ull << (dev & 63);
   if (!(configured.load(std::memory_order_acquire) & bit)) {
-    e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE, NDF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(glint_eval_kernel<DEBUG, TMA, MODE, NDF, KAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return e;
     configured.fetch_or(bit, std::memory_order_release);
   }
   if (!pdl) {
-    glint_eval_kernel<DEBUG, TMA, MODE, NDF><<<grid, kBlock, smem, stream>>>(prm);
+    glint_eval_kernel<DEBUG, TMA, MODE, NDF, KAT><<<grid, kBlock, smem, stream>>>(prm);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -1021,7 +1021,7 @@ static cudaError_t launch_t(const KParams& prm, int grid, cudaStream_t stream, b
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, glint_eval_kernel<DEBUG, TMA, MODE, NDF>, prm);
+  return cudaLaunchKernelEx(&cfg, glint_eval_kernel<DEBUG, TMA, MODE, NDF, KAT>, prm);
 }
 
 cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t stream, bool pdl) {
@@ -1029,14 +1029,25 @@ cudaError_t launch_eval(const KParams& prm, int grid, bool debug, cudaStream_t s
                                                   (uintptr_t)prm.pos | (uintptr_t)prm.mat) % 16 == 0);
   if (debug)
     return tma ? launch_t<true, true, 0>(prm, grid, stream, pdl) : launch_t<true, false, 0>(prm, grid, stream, pdl);
+  // the angular node-seed table (see g_sKA) pays with several lights; with one
+  // light the four independent hash chains hide better than its LDS latency
+  // (C2 -0.4 % with the table), and small beta would overflow it
+  const bool kat = GLINT_KA_TABLE && prm.sc.n_lights >= 2 && 1.0f / prm.sc.beta <= 29.0f;
   switch (prm.sc.eval_mode) {
     case 1:
+      if (kat) return tma ? launch_t<false, true, 1, -1, true>(prm, grid, stream, pdl) : launch_t<false, false, 1, -1, true>(prm, grid, stream, pdl);
       return tma ? launch_t<false, true, 1>(prm, grid, stream, pdl) : launch_t<false, false, 1>(prm, grid, stream, pdl);
     case 2:
+      if (kat) return tma ? launch_t<false, true, 2, -1, true>(prm, grid, stream, pdl) : launch_t<false, false, 2, -1, true>(prm, grid, stream, pdl);
       return tma ? launch_t<false, true, 2>(prm, grid, stream, pdl) : launch_t<false, false, 2>(prm, grid, stream, pdl);
     case 3:
       return tma ? launch_t<false, true, 3>(prm, grid, stream, pdl) : launch_t<false, false, 3>(prm, grid, stream, pdl);
     default:
+      if (kat) {
+        if (prm.sc.ndf_kind == 0)
+          return tma ? launch_t<false, true, 0, 0, true>(prm, grid, stream, pdl) : launch_t<false, false, 0, 0, true>(prm, grid, stream, pdl);
+        return tma ? launch_t<false, true, 0, 1, true>(prm, grid, stream, pdl) : launch_t<false, false, 0, 1, true>(prm, grid, stream, pdl);
+      }
       if (prm.sc.ndf_kind == 0)
         return tma ? launch_t<false, true, 0, 0>(prm, grid, stream, pdl) : launch_t<false, false, 0, 0>(prm, grid, stream, pdl);
       return tma ? launch_t<false, true, 0, 1>(prm, grid, stream, pdl) : launch_t<false, false, 0, 1>(prm, grid, stream, pdl);
@@ -1084,10 +1095,10 @@ cudaError_t launch_count_active(const float4* duv, const float4* uvm, const floa
 }
 
 cudaError_t occupancy_blocks_per_sm(int* out) {
-  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true, 0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(glint_eval_kernel<false, true, 0, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kSmemTma);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true, 0, 0>, kBlock, kSmemTma);
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, glint_eval_kernel<false, true, 0, 0, false>, kBlock, kSmemTma);
 }
 
 }  // namespace glint
